@@ -1,0 +1,230 @@
+/*
+ * refusion_b200.h -- C ABI of the B200-native surface-correction hot path.
+ *
+ * Drop-in boundary for the reference package `refusion` (arXiv 1709.03763):
+ * the reference's plugin point is the kernel backend `refusion.kernels`
+ * (src/refusion/kernels.py:19-41, selected by REFUSION_BACKEND) and the
+ * volume API it serves (src/refusion/volume.py).  Every entry point below
+ * names the reference function it replaces.  Paths are relative to
+ * /root/reference/pkg/.
+ *
+ * Conventions
+ *  - Plain C types only; every call returns an rf_status.
+ *  - Keyframe planes (rf_kf_view) are DEVICE pointers owned by the caller;
+ *    they must stay alive until the call returns (calls that return
+ *    results synchronise the volume's stream; rf_stream_async does not).
+ *  - Host buffers (keys, exported blocks) are plain host memory.
+ *  - One volume-mutating call at a time per rf_volume; calls are
+ *    ordered on the volume's CUDA stream (rf_set_cuda_stream).
+ *  - Block keys pack (bx, by, bz) as ((bx+2^20)<<42)|((by+2^20)<<21)|(bz+2^20)
+ *    (src/refusion/volume.py:137-148).
+ *  - Exported / imported block records are 5 planes of 512 doubles:
+ *    D, W, C0, C1, C2 with voxel index l = x + 8y + 64z
+ *    (src/refusion/volume.py:69-81).
+ */
+#ifndef REFUSION_B200_H
+#define REFUSION_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum rf_status {
+    RF_OK = 0,
+    RF_STREAMING_CONTRACT = 1,  /* errors.StreamingContractError (src/refusion/errors.py:20) */
+    RF_INCONSISTENT = 2,        /* errors.VolumeInconsistencyError (src/refusion/errors.py:24) */
+    RF_CAPACITY = 3,            /* block pool exhausted */
+    RF_INVALID_ARG = 4,         /* ValueError */
+    RF_CUDA = 5                 /* CUDA runtime failure */
+} rf_status;
+
+typedef struct rf_volume rf_volume;
+
+/* VolumeConfig (src/refusion/volume.py:39-66) plus device sizing. */
+typedef struct rf_config {
+    double voxel_size;       /* metres */
+    double mu;               /* truncation band */
+    double stream_radius;    /* active-sphere radius */
+    int64_t hash_buckets;    /* bucket count of block_hash (any > 0) */
+    int64_t block_capacity;  /* max resident blocks (20,480 B each) */
+    int32_t device;          /* CUDA device ordinal */
+    int32_t shard_rank;      /* this GPU's shard (0 when unsharded) */
+    int32_t shard_count;     /* number of shards (1 when unsharded) */
+    int32_t max_pixels;      /* largest keyframe width*height (0 -> 640*480) */
+} rf_config;
+
+/* Pose (src/refusion/geometry.py:41-62): p_world = R p_cam + t, R row-major. */
+typedef struct rf_pose {
+    double R[9];
+    double t[3];
+} rf_pose;
+
+/* Duck-typed keyframe (reference tests/test_volume.py:12-20). */
+typedef struct rf_kf_view {
+    const double *depth;   /* [height][width] device */
+    const double *weight;  /* [height][width] device */
+    const double *color;   /* [height][width][3] device, or NULL (zeros, volume.py:256-259) */
+    int32_t width, height;
+    double fx, fy, cx, cy;
+} rf_kf_view;
+
+/* IntegrationRecord counts (src/refusion/volume.py:126-134). */
+typedef struct rf_op_result {
+    int64_t blocks_touched;
+    int64_t voxels_updated;
+    int64_t n_new;
+} rf_op_result;
+
+/* stream() return dict (src/refusion/volume.py:375-379). */
+typedef struct rf_stream_result {
+    int64_t streamed_in;
+    int64_t streamed_out;
+    int64_t relocated;
+} rf_stream_result;
+
+/* TwoTierStore counters (src/refusion/volume.py:104-110). */
+typedef struct rf_counters {
+    int64_t blocks_streamed_in;
+    int64_t blocks_streamed_out;
+    int64_t sphere_relocations;
+    int64_t block_count;
+    int64_t active_count;      /* blocks inside the sphere around last_center */
+    int32_t has_center;
+    int32_t _pad;
+    double last_center[3];
+} rf_counters;
+
+/* One batched pose-graph correction (reintegration.py:156-181). */
+typedef struct rf_window_result {
+    int32_t status;          /* rf_status of the window */
+    int32_t failed_entry;    /* entry index that raised, -1 if none */
+    int32_t failed_phase;    /* 0 de-integration, 1 integration, -1 none */
+    int32_t _pad;
+    int64_t n_corrected;     /* entries re-integrated (0 on error) */
+    int64_t voxels_updated;  /* summed over the integrate phase */
+    int64_t blocks_touched;  /* summed over all (de)integrations */
+    int64_t n_new;           /* blocks allocated during the window */
+    int64_t gc_freed;        /* blocks dropped by the closing GC */
+} rf_window_result;
+
+/* Device-side timing of the hot kernels (CUDA events on the volume's stream). */
+typedef struct rf_profile {
+    int64_t fuse_launches;       /* integrate/de-integrate apply kernels */
+    double fuse_ms;              /* summed device time of those launches */
+    int64_t check_launches;      /* de-integration check kernels */
+    double check_ms;
+    int64_t footprint_launches;  /* footprint + allocation kernels */
+    double footprint_ms;
+    int64_t voxels_updated;      /* voxels written by profiled fuse launches */
+    int64_t pixels;              /* keyframe pixels read by profiled fuse launches */
+    int64_t blocks_touched;
+    int64_t kernel_launches;     /* every kernel this library launched while profiling */
+} rf_profile;
+
+/* ---- lifecycle ------------------------------------------------------- */
+/* TwoTierStore() (volume.py:96-110) */
+rf_status rf_volume_create(const rf_config *cfg, rf_volume **out);
+rf_status rf_volume_destroy(rf_volume *vol);
+/* stream is a cudaStream_t (NULL = legacy default stream) */
+rf_status rf_set_cuda_stream(rf_volume *vol, void *stream);
+const char *rf_last_error(const rf_volume *vol);
+const char *rf_status_string(int status);
+
+/* ---- hashing ----------------------------------------------------------- */
+/* block_hash (volume.py:84-93): XOR of prime products, floor-mod buckets */
+int64_t rf_block_hash(int64_t x, int64_t y, int64_t z, int64_t buckets);
+/* shard owning a packed key (multi-GPU hash sharding) */
+int32_t rf_key_owner(int64_t key, int32_t shard_count);
+
+/* ---- volume operations --------------------------------------------- */
+/* stream (volume.py:351-379).  result may be NULL: then nothing syncs. */
+rf_status rf_stream(rf_volume *vol, const double center[3], rf_stream_result *result);
+/* keyframe_block_footprint (volume.py:151-197): sorted unique keys, no allocation.
+ * *n_out receives the count; if it exceeds cap nothing is written past cap. */
+rf_status rf_footprint(rf_volume *vol, const rf_kf_view *kf, const rf_pose *pose,
+                       int64_t *keys_host, int64_t cap, int64_t *n_out);
+/* allocate_blocks (volume.py:216-249): new keys (unsorted) into keys_host. */
+rf_status rf_allocate(rf_volume *vol, const rf_kf_view *kf, const rf_pose *pose,
+                      int64_t *new_keys_host, int64_t cap, int64_t *n_new);
+/* integrate (volume.py:296-312); new_keys_host may be NULL. */
+rf_status rf_integrate(rf_volume *vol, const rf_kf_view *kf, const rf_pose *pose,
+                       rf_op_result *result, int64_t *new_keys_host, int64_t new_cap);
+/* deintegrate (volume.py:315-338); all-or-nothing as the reference. */
+rf_status rf_deintegrate(rf_volume *vol, const rf_kf_view *kf, const rf_pose *pose,
+                         rf_op_result *result);
+/* reintegration._correct_entries (reintegration.py:156-181) for m entries,
+ * followed by stream(next_center) when next_center != NULL
+ * (correct_window / correct_topk, reintegration.py:184-209).  One host
+ * synchronisation per call. */
+rf_status rf_correct(rf_volume *vol, int32_t m, const rf_kf_view *kfs,
+                     const rf_pose *old_poses, const rf_pose *new_poses,
+                     const double *next_center, rf_window_result *result);
+/* garbage_collect (volume.py:382-390) */
+rf_status rf_garbage_collect(rf_volume *vol, int64_t *freed);
+/* total_weight (volume.py:393-394) */
+rf_status rf_total_weight(rf_volume *vol, double *out);
+rf_status rf_counters_get(rf_volume *vol, rf_counters *out);
+
+/* ---- snapshots / parity (volume.py:397-464) --------------------------- */
+/* keys [n], data [n][5][512] doubles (D, W, C0, C1, C2); slot order. */
+rf_status rf_export_blocks(rf_volume *vol, int64_t *keys_host, double *data_host,
+                           int64_t cap, int64_t *n_out);
+/* insert blocks with the given contents (load_volume, volume.py:418-442) */
+rf_status rf_import_blocks(rf_volume *vol, const int64_t *keys_host,
+                           const double *data_host, int64_t n);
+/* read back selected blocks by key; missing blocks -> found[i] = 0 */
+rf_status rf_read_blocks(rf_volume *vol, const int64_t *keys_host, int64_t n,
+                         double *data_host, int32_t *found_host);
+
+/* ---- the reference kernel plugin point --------------------------------- */
+/* kernels.fuse_block (src/refusion/_kernels_cy.pyx:14-108): one block, HOST
+ * arrays, same argument meaning and in-place semantics; runs the same
+ * device code as rf_integrate.  *count_out = voxels updated or -1. */
+rf_status rf_fuse_block(double *d, double *w, double *c,
+                        double ox, double oy, double oz, double voxel_size,
+                        const double *rot_wc, double tx, double ty, double tz,
+                        double fx, double fy, double cx, double cy,
+                        int32_t width, int32_t height,
+                        const double *kf_depth, const double *kf_weight,
+                        const double *kf_color, double mu, double eps_w,
+                        int32_t remove, int32_t *count_out);
+
+/* ---- measurement -------------------------------------------------------- */
+rf_status rf_profile_begin(rf_volume *vol);
+rf_status rf_profile_end(rf_volume *vol, rf_profile *out);
+
+/* ---- synthetic data (measurement infrastructure, synth.py:46-283) ------ */
+typedef struct rf_synth_prim {
+    int32_t kind;        /* 0 Sphere (size[0] = radius), 1 BoxSolid, 2 RoomShell */
+    int32_t _pad;
+    double center[3];
+    double size[3];      /* half extents (box / room) */
+    double albedo[3];
+} rf_synth_prim;
+
+typedef struct rf_synth_params {
+    double z_max;        /* synth.py:29 */
+    double tol;          /* SPHERE_TRACE_TOL */
+    double sigma0;       /* depth noise sigma0 * z^2 (0 = none) */
+    double ambient, diffuse;
+    double light[3];     /* unit light direction */
+    uint64_t seed;
+    int32_t steps;       /* SPHERE_TRACE_STEPS */
+    int32_t _pad;
+} rf_synth_params;
+
+/* Render z-depth [h][w] and colour [h][w][3] (colour may be NULL) of an
+ * analytic scene; prims, depth and colour are device pointers. */
+rf_status rf_synth_render(const rf_synth_prim *prims_dev, int32_t n_prims,
+                          const rf_pose *pose, double fx, double fy, double cx,
+                          double cy, int32_t width, int32_t height,
+                          const rf_synth_params *params, double *depth_dev,
+                          double *color_dev, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REFUSION_B200_H */

@@ -1,0 +1,209 @@
+"""ctypes binding of the C ABI in include/refusion_b200.h.
+
+The shared library ``librefusion_b200.so`` (built in-tree by
+``__graft_entry__.build()``) holds every CUDA kernel of the hot path.  There
+is no fallback: if the library or a CUDA device is missing, ``lib()`` raises
+so that nothing silently runs on the CPU.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librefusion_b200.so")
+
+RF_OK = 0
+RF_STREAMING_CONTRACT = 1
+RF_INCONSISTENT = 2
+RF_CAPACITY = 3
+RF_INVALID_ARG = 4
+RF_CUDA = 5
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+c_int64_p = ctypes.POINTER(ctypes.c_int64)
+c_int32_p = ctypes.POINTER(ctypes.c_int32)
+
+
+class RfConfig(ctypes.Structure):
+    _fields_ = [
+        ("voxel_size", ctypes.c_double),
+        ("mu", ctypes.c_double),
+        ("stream_radius", ctypes.c_double),
+        ("hash_buckets", ctypes.c_int64),
+        ("block_capacity", ctypes.c_int64),
+        ("device", ctypes.c_int32),
+        ("shard_rank", ctypes.c_int32),
+        ("shard_count", ctypes.c_int32),
+        ("max_pixels", ctypes.c_int32),
+    ]
+
+
+class RfPose(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_double * 9), ("t", ctypes.c_double * 3)]
+
+
+class RfKfView(ctypes.Structure):
+    _fields_ = [
+        ("depth", ctypes.c_void_p),
+        ("weight", ctypes.c_void_p),
+        ("color", ctypes.c_void_p),
+        ("width", ctypes.c_int32),
+        ("height", ctypes.c_int32),
+        ("fx", ctypes.c_double),
+        ("fy", ctypes.c_double),
+        ("cx", ctypes.c_double),
+        ("cy", ctypes.c_double),
+    ]
+
+
+class RfOpResult(ctypes.Structure):
+    _fields_ = [
+        ("blocks_touched", ctypes.c_int64),
+        ("voxels_updated", ctypes.c_int64),
+        ("n_new", ctypes.c_int64),
+    ]
+
+
+class RfStreamResult(ctypes.Structure):
+    _fields_ = [
+        ("streamed_in", ctypes.c_int64),
+        ("streamed_out", ctypes.c_int64),
+        ("relocated", ctypes.c_int64),
+    ]
+
+
+class RfCounters(ctypes.Structure):
+    _fields_ = [
+        ("blocks_streamed_in", ctypes.c_int64),
+        ("blocks_streamed_out", ctypes.c_int64),
+        ("sphere_relocations", ctypes.c_int64),
+        ("block_count", ctypes.c_int64),
+        ("active_count", ctypes.c_int64),
+        ("has_center", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("last_center", ctypes.c_double * 3),
+    ]
+
+
+class RfWindowResult(ctypes.Structure):
+    _fields_ = [
+        ("status", ctypes.c_int32),
+        ("failed_entry", ctypes.c_int32),
+        ("failed_phase", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("n_corrected", ctypes.c_int64),
+        ("voxels_updated", ctypes.c_int64),
+        ("blocks_touched", ctypes.c_int64),
+        ("n_new", ctypes.c_int64),
+        ("gc_freed", ctypes.c_int64),
+    ]
+
+
+class RfProfile(ctypes.Structure):
+    _fields_ = [
+        ("fuse_launches", ctypes.c_int64),
+        ("fuse_ms", ctypes.c_double),
+        ("check_launches", ctypes.c_int64),
+        ("check_ms", ctypes.c_double),
+        ("footprint_launches", ctypes.c_int64),
+        ("footprint_ms", ctypes.c_double),
+        ("voxels_updated", ctypes.c_int64),
+        ("pixels", ctypes.c_int64),
+        ("blocks_touched", ctypes.c_int64),
+        ("kernel_launches", ctypes.c_int64),
+    ]
+
+
+class RfSynthPrim(ctypes.Structure):
+    _fields_ = [
+        ("kind", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+        ("center", ctypes.c_double * 3),
+        ("size", ctypes.c_double * 3),
+        ("albedo", ctypes.c_double * 3),
+    ]
+
+
+class RfSynthParams(ctypes.Structure):
+    _fields_ = [
+        ("z_max", ctypes.c_double),
+        ("tol", ctypes.c_double),
+        ("sigma0", ctypes.c_double),
+        ("ambient", ctypes.c_double),
+        ("diffuse", ctypes.c_double),
+        ("light", ctypes.c_double * 3),
+        ("seed", ctypes.c_uint64),
+        ("steps", ctypes.c_int32),
+        ("_pad", ctypes.c_int32),
+    ]
+
+
+_vp = ctypes.c_void_p
+_S = ctypes.c_int  # rf_status
+
+# name -> (restype, argtypes); exactly the symbols include/refusion_b200.h declares
+SIGNATURES = {
+    "rf_volume_create": (_S, [ctypes.POINTER(RfConfig), ctypes.POINTER(_vp)]),
+    "rf_volume_destroy": (_S, [_vp]),
+    "rf_set_cuda_stream": (_S, [_vp, _vp]),
+    "rf_last_error": (ctypes.c_char_p, [_vp]),
+    "rf_status_string": (ctypes.c_char_p, [ctypes.c_int]),
+    "rf_block_hash": (ctypes.c_int64, [ctypes.c_int64] * 4),
+    "rf_key_owner": (ctypes.c_int32, [ctypes.c_int64, ctypes.c_int32]),
+    "rf_stream": (_S, [_vp, c_double_p, ctypes.POINTER(RfStreamResult)]),
+    "rf_footprint": (_S, [_vp, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose), c_int64_p,
+                          ctypes.c_int64, c_int64_p]),
+    "rf_allocate": (_S, [_vp, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose), c_int64_p,
+                         ctypes.c_int64, c_int64_p]),
+    "rf_integrate": (_S, [_vp, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
+                          ctypes.POINTER(RfOpResult), c_int64_p, ctypes.c_int64]),
+    "rf_deintegrate": (_S, [_vp, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
+                            ctypes.POINTER(RfOpResult)]),
+    "rf_correct": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
+                        ctypes.POINTER(RfPose), c_double_p, ctypes.POINTER(RfWindowResult)]),
+    "rf_garbage_collect": (_S, [_vp, c_int64_p]),
+    "rf_total_weight": (_S, [_vp, c_double_p]),
+    "rf_counters_get": (_S, [_vp, ctypes.POINTER(RfCounters)]),
+    "rf_export_blocks": (_S, [_vp, c_int64_p, c_double_p, ctypes.c_int64, c_int64_p]),
+    "rf_import_blocks": (_S, [_vp, c_int64_p, c_double_p, ctypes.c_int64]),
+    "rf_read_blocks": (_S, [_vp, c_int64_p, ctypes.c_int64, c_double_p, c_int32_p]),
+    "rf_fuse_block": (_S, [c_double_p, c_double_p, c_double_p] + [ctypes.c_double] * 4
+                      + [c_double_p] + [ctypes.c_double] * 7 + [ctypes.c_int32] * 2
+                      + [c_double_p] * 3 + [ctypes.c_double] * 2
+                      + [ctypes.c_int32, c_int32_p]),
+    "rf_profile_begin": (_S, [_vp]),
+    "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
+    "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4
+                        + [ctypes.c_int32] * 2 + [ctypes.POINTER(RfSynthParams), _vp, _vp, _vp]),
+}
+
+_lib = None
+
+
+def load_library(path=LIB_PATH):
+    """Load and type the shared library without touching any CUDA device."""
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (there is no CPU fallback)"
+        )
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+def lib():
+    """The typed library; raises if it is absent or no CUDA device exists."""
+    global _lib
+    if _lib is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError(
+                "paper_1709_03763_b200 needs a CUDA device (B200); no CPU fallback exists"
+            )
+        _lib = load_library()
+    return _lib

@@ -1,0 +1,960 @@
+// rf_volume.cu -- host side of the C ABI (include/refusion_b200.h): device
+// state of one sparse voxel-hashed TSDF shard and the op sequencer that turns
+// the reference's volume calls into stream-ordered kernel launches.
+//
+// Reference behaviour followed (paths under /root/reference/pkg/src/refusion):
+//   volume.py:151-197  keyframe_block_footprint  -> k_footprint
+//   volume.py:216-249  allocate_blocks           -> k_footprint (+ k_fuse fix-up)
+//   volume.py:296-338  integrate / deintegrate   -> k_fuse<...>
+//   volume.py:341-379  stream                    -> k_stream (+ host centre/relocations)
+//   volume.py:382-394  garbage_collect/total_weight
+//   reintegration.py:156-223 _correct_entries    -> rf_correct (one sync per window)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "refusion_b200.h"
+#include "rf_kernels.cuh"
+
+using namespace rf;
+
+namespace {
+
+constexpr int kMaxWindowOps = 4096;
+// distinct new blocks one (de)integration may create (load factor stays low)
+constexpr int kPendingSlots = 1 << 20;
+
+struct EventPair {
+  cudaEvent_t a, b;
+  int kind;  // 0 fuse, 1 check, 2 footprint
+};
+
+}  // namespace
+
+struct rf_volume {
+  rf_config cfg{};
+  cudaStream_t stream = nullptr;
+  Table T{};
+  OpCounters* d_ops = nullptr;
+  OpCounters* h_ops = nullptr;  // pinned
+  int ops_cap = 0;
+  WinState* d_ws = nullptr;
+  WinState* h_ws = nullptr;  // pinned
+  unsigned long long* d_u64 = nullptr;  // scratch counters [8]
+  unsigned long long* h_u64 = nullptr;  // pinned [8]
+  double* d_wsums = nullptr;
+  double* d_f64 = nullptr;
+  double* h_f64 = nullptr;
+  AllocState* h_alloc = nullptr;  // pinned
+  // host mirror of the streaming state (volume.py:104-110)
+  bool has_center = false;
+  double center[3] = {0, 0, 0};
+  long long relocations = 0;
+  unsigned epoch = 0;
+  int n_sms = 148;
+  int fuse_grid = 148 * 2;
+  int fp_grid_cap = 148 * 8;
+  // profiling
+  bool profiling = false;
+  std::vector<EventPair> events;
+  std::vector<cudaEvent_t> event_pool;
+  long long prof_voxels = 0, prof_pixels = 0, prof_blocks = 0, prof_launches = 0;
+  std::string err;
+};
+
+namespace {
+
+rf_status fail(rf_volume* v, rf_status st, const std::string& msg) {
+  if (v) v->err = msg;
+  return st;
+}
+
+#define RF_CUDA_TRY(v, expr)                                                          \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail((v), RF_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+cudaEvent_t take_event(rf_volume* v) {
+  if (!v->event_pool.empty()) {
+    cudaEvent_t e = v->event_pool.back();
+    v->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+struct ProfScope {
+  rf_volume* v;
+  int kind;
+  cudaEvent_t a = nullptr;
+  ProfScope(rf_volume* v_, int k) : v(v_), kind(k) {
+    if (v->profiling) {
+      a = take_event(v);
+      cudaEventRecord(a, v->stream);
+    }
+  }
+  ~ProfScope() {
+    if (a) {
+      cudaEvent_t b = take_event(v);
+      cudaEventRecord(b, v->stream);
+      v->events.push_back({a, b, kind});
+    }
+  }
+};
+
+KfView to_view(const rf_kf_view* kf) {
+  KfView k;
+  k.depth = kf->depth;
+  k.weight = kf->weight;
+  k.color = kf->color;
+  k.width = kf->width;
+  k.height = kf->height;
+  k.fx = kf->fx;
+  k.fy = kf->fy;
+  k.cx = kf->cx;
+  k.cy = kf->cy;
+  return k;
+}
+
+bool valid_kf(const rf_kf_view* kf) {
+  return kf && kf->depth && kf->weight && kf->width > 0 && kf->height > 0 &&
+         static_cast<long long>(kf->width) * kf->height < (1LL << 31);
+}
+
+// One batch of device ops sharing a single host synchronisation.
+struct PendingStream {
+  int op;
+  double c[3];
+  int relocated;
+};
+
+struct OpInfo {
+  int kind;  // 0 stream, 1 integrate, 2 deintegrate, 3 gc, 4 allocate
+  int entry;
+};
+
+struct Batch {
+  rf_volume* v;
+  int n_ops = 0;
+  bool has_center;
+  double center[3];
+  std::vector<PendingStream> streams;
+  std::vector<OpInfo> infos;
+  int gc_op = -1;
+};
+
+rf_status ensure_ops(rf_volume* v, int n) {
+  if (n <= v->ops_cap) return RF_OK;
+  if (v->d_ops) cudaFree(v->d_ops);
+  if (v->h_ops) cudaFreeHost(v->h_ops);
+  v->ops_cap = std::max(n, 64);
+  RF_CUDA_TRY(v, cudaMalloc(&v->d_ops, sizeof(OpCounters) * v->ops_cap));
+  RF_CUDA_TRY(v, cudaMallocHost(&v->h_ops, sizeof(OpCounters) * v->ops_cap));
+  return RF_OK;
+}
+
+rf_status batch_begin(rf_volume* v, Batch& b, int max_ops) {
+  if (max_ops > kMaxWindowOps * 8) return fail(v, RF_INVALID_ARG, "too many ops in one call");
+  rf_status st = ensure_ops(v, max_ops);
+  if (st != RF_OK) return st;
+  b.v = v;
+  b.has_center = v->has_center;
+  std::memcpy(b.center, v->center, sizeof(b.center));
+  const int n = std::max(max_ops, 1);
+  k_reset_ops<<<(n + 127) / 128, 128, 0, v->stream>>>(v->d_ops, n, v->d_ws);
+  if (v->profiling) v->prof_launches += 1;
+  return RF_OK;
+}
+
+void op_stream(Batch& b, const double c[3]) {
+  rf_volume* v = b.v;
+  const int op = b.n_ops++;
+  b.infos.push_back({0, -1});
+  StreamParams p{};
+  std::memcpy(p.old_c, b.center, sizeof(p.old_c));
+  std::memcpy(p.new_c, c, sizeof(p.new_c));
+  p.has_old = b.has_center;
+  p.span = kBlockSide * v->cfg.voxel_size;
+  p.radius = v->cfg.stream_radius;
+  p.op_index = op;
+  p.op = v->d_ops + op;
+  p.ws = v->d_ws;
+  k_stream<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, p);
+  if (v->profiling) v->prof_launches += 1;
+  // relocation (volume.py:358-364): centre moved more than one block span
+  int reloc = 0;
+  if (b.has_center) {
+    const double dx = c[0] - b.center[0], dy = c[1] - b.center[1], dz = c[2] - b.center[2];
+    const double moved = std::sqrt(dx * dx + dy * dy + dz * dz);
+    if (moved > kBlockSide * v->cfg.voxel_size) reloc = 1;
+  }
+  b.streams.push_back({op, {c[0], c[1], c[2]}, reloc});
+  b.has_center = true;
+  std::memcpy(b.center, c, sizeof(b.center));
+}
+
+FootprintParams footprint_params(rf_volume* v, const Batch& b, const rf_kf_view* kf,
+                                 const rf_pose* pose, int op) {
+  FootprintParams p{};
+  p.kf = to_view(kf);
+  std::memcpy(p.R, pose->R, sizeof(p.R));
+  std::memcpy(p.t, pose->t, sizeof(p.t));
+  p.voxel_size = v->cfg.voxel_size;
+  p.mu = v->cfg.mu;
+  p.span = kBlockSide * v->cfg.voxel_size;
+  p.inv_span = 1.0 / p.span;                       // volume.py:177
+  p.min_z = 0.25 * v->cfg.voxel_size;              // volume.py:30, :170
+  p.radius = v->cfg.stream_radius;
+  std::memcpy(p.center, b.center, sizeof(p.center));
+  p.has_center = b.has_center;
+  p.n_steps = static_cast<int>(std::ceil(2.0 * v->cfg.mu / v->cfg.voxel_size)) + 1;  // :172
+  p.shard_rank = v->cfg.shard_rank;
+  p.shard_count = v->cfg.shard_count;
+  p.epoch = ++v->epoch;
+  if (v->epoch == 0xffffffffu) v->epoch = 1;  // stamps are reset lazily: 0 is "never"
+  p.op_index = op;
+  p.op = v->d_ops + op;
+  p.ws = v->d_ws;
+  return p;
+}
+
+FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, int op) {
+  FuseParams p{};
+  p.kf = to_view(kf);
+  // rot_wc = pose.rotation.T (volume.py:260)
+  for (int r = 0; r < 3; ++r)
+    for (int c = 0; c < 3; ++c) p.Rwc[3 * r + c] = pose->R[3 * c + r];
+  std::memcpy(p.t, pose->t, sizeof(p.t));
+  p.voxel_size = v->cfg.voxel_size;
+  p.span = kBlockSide * v->cfg.voxel_size;
+  p.mu = v->cfg.mu;
+  p.eps_w = 1e-9;  // EPS_W, volume.py:26
+  p.op_index = op;
+  p.op = v->d_ops + op;
+  p.ws = v->d_ws;
+  return p;
+}
+
+int footprint_grid(rf_volume* v, const rf_kf_view* kf) {
+  const long long npix = static_cast<long long>(kf->width) * kf->height;
+  return static_cast<int>(std::max(1LL, std::min<long long>((npix + 255) / 256, v->fp_grid_cap)));
+}
+
+// mode: 0 integrate, 1 deintegrate, 2 allocate only
+void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
+  rf_volume* v = b.v;
+  const int op = b.n_ops++;
+  b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
+  FootprintParams fp = footprint_params(v, b, kf, pose, op);
+  {
+    ProfScope ps(v, 2);
+    k_footprint<false><<<footprint_grid(v, kf), 256, 0, v->stream>>>(v->T, fp);
+    k_commit<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
+  }
+  FuseParams p = fuse_params(v, kf, pose, op);
+  if (mode == 2) {
+    p.alloc_only = 1;
+    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    return;
+  }
+  if (mode == 0) {
+    ProfScope ps(v, 0);
+    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+  } else {
+    {
+      ProfScope ps(v, 1);
+      k_fuse<kCheckRemove><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    }
+    ProfScope ps(v, 0);
+    k_fuse<kApplyRemove><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+  }
+  if (v->profiling) {
+    v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
+    v->prof_launches += mode == 1 ? 4 : 3;
+  }
+}
+
+void op_gc(Batch& b) {
+  rf_volume* v = b.v;
+  const int op = b.n_ops++;
+  b.infos.push_back({3, -1});
+  b.gc_op = op;
+  const long long grid = std::min<long long>((v->cfg.hash_buckets + 255) / 256, v->n_sms * 8);
+  // freed count lands in the op's n_new field
+  k_gc<<<static_cast<int>(std::max(1LL, grid)), 256, 0, v->stream>>>(
+      v->T, op, v->d_ws, &v->d_ops[op].n_new);
+  if (v->profiling) v->prof_launches += 1;
+}
+
+struct BatchOutcome {
+  int err_kind = kErrNone;
+  int err_op = -1;
+};
+
+// Synchronise once, read every op record, commit host streaming state for
+// the ops that executed.
+rf_status batch_end(Batch& b, BatchOutcome& out) {
+  rf_volume* v = b.v;
+  const int n = std::max(b.n_ops, 1);
+  cudaMemcpyAsync(v->h_ops, v->d_ops, sizeof(OpCounters) * n, cudaMemcpyDeviceToHost, v->stream);
+  cudaMemcpyAsync(v->h_ws, v->d_ws, sizeof(WinState), cudaMemcpyDeviceToHost, v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  RF_CUDA_TRY(v, cudaGetLastError());
+  out.err_kind = v->h_ws->err_kind;
+  out.err_op = out.err_kind ? v->h_ws->err_op : -1;
+  for (const PendingStream& s : b.streams) {
+    if (out.err_kind && s.op > out.err_op) break;
+    v->has_center = true;
+    std::memcpy(v->center, s.c, sizeof(v->center));
+    v->relocations += s.relocated;
+  }
+  if (v->profiling) {
+    for (int i = 0; i < b.n_ops; ++i) {
+      const int k = b.infos[i].kind;
+      if ((k == 1 || k == 2) && (!out.err_kind || i < out.err_op)) {
+        v->prof_voxels += static_cast<long long>(v->h_ops[i].voxels_updated);
+        v->prof_blocks += static_cast<long long>(v->h_ops[i].n_touched);
+      }
+    }
+  }
+  return RF_OK;
+}
+
+rf_status status_of(rf_volume* v, int err_kind, const char* what) {
+  switch (err_kind) {
+    case kErrNone: return RF_OK;
+    case kErrContract:
+      return fail(v, RF_STREAMING_CONTRACT,
+                  std::string(what) + ": a footprint block lies outside the active streaming "
+                                      "sphere (host tier or beyond stream_radius), or stream() "
+                                      "was never positioned");
+    case kErrInconsistent:
+      return fail(v, RF_INCONSISTENT,
+                  std::string(what) + ": de-integration would drive a weight negative; the "
+                                      "keyframe was not integrated with this pose");
+    case kErrCapacity:
+      return fail(v, RF_CAPACITY, std::string(what) + ": block pool capacity exhausted");
+  }
+  return fail(v, RF_CUDA, "unknown device error");
+}
+
+rf_status copy_new_keys(rf_volume* v, int op, int64_t* keys_host, int64_t cap) {
+  const long long n = static_cast<long long>(v->h_ops[op].n_new);
+  if (!keys_host || n == 0) return RF_OK;
+  const long long m = std::min<long long>(n, cap);
+  long long* d_keys = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_keys, sizeof(long long) * m + 8, v->stream));
+  k_gather_keys<<<static_cast<int>((m + 255) / 256), 256, 0, v->stream>>>(v->T, v->T.new_list, m, d_keys);
+  cudaMemcpyAsync(keys_host, d_keys, sizeof(long long) * m, cudaMemcpyDeviceToHost, v->stream);
+  cudaFreeAsync(d_keys, v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  return RF_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+const char* rf_status_string(int status) {
+  switch (status) {
+    case RF_OK: return "ok";
+    case RF_STREAMING_CONTRACT: return "streaming contract violated";
+    case RF_INCONSISTENT: return "volume inconsistency";
+    case RF_CAPACITY: return "block capacity exhausted";
+    case RF_INVALID_ARG: return "invalid argument";
+    case RF_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* rf_last_error(const rf_volume* vol) { return vol ? vol->err.c_str() : ""; }
+
+int64_t rf_block_hash(int64_t x, int64_t y, int64_t z, int64_t buckets) {
+  if (buckets <= 0) return -1;
+  return block_hash(x, y, z, buckets);
+}
+
+int32_t rf_key_owner(int64_t key, int32_t shard_count) {
+  return shard_count <= 1 ? 0 : key_owner(key, shard_count);
+}
+
+rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
+  if (!cfg || !out) return RF_INVALID_ARG;
+  *out = nullptr;
+  if (!(cfg->voxel_size > 0.0) || !(cfg->mu >= 2.0 * cfg->voxel_size) ||
+      !(cfg->stream_radius > cfg->mu) || cfg->hash_buckets <= 0 ||
+      cfg->hash_buckets > 0x7fffffffLL || cfg->block_capacity <= 0 ||
+      cfg->block_capacity > 0x7ffffff0LL || cfg->shard_count < 1 || cfg->shard_rank < 0 ||
+      cfg->shard_rank >= cfg->shard_count)
+    return RF_INVALID_ARG;
+  rf_volume* v = new rf_volume();
+  v->cfg = *cfg;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) {
+    delete v;
+    return RF_CUDA;
+  }
+  cudaDeviceGetAttribute(&v->n_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  int occ = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse<kIntegrate>, kFuseThreads, 0);
+  v->fuse_grid = v->n_sms * std::max(occ, 1);
+  v->fp_grid_cap = v->n_sms * 8;
+  const size_t cap = static_cast<size_t>(cfg->block_capacity);
+  Table& T = v->T;
+  T.buckets = cfg->hash_buckets;
+  T.capacity = static_cast<int>(cap);
+  T.pend_mask = kPendingSlots - 1;
+  auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes) == cudaSuccess; };
+  bool ok = alloc(reinterpret_cast<void**>(&T.heads), sizeof(int) * cfg->hash_buckets) &&
+            alloc(reinterpret_cast<void**>(&T.keys), sizeof(long long) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.next), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.nz), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.stamp), sizeof(unsigned) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.free_stack), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.returned), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.touched), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.new_list), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.pend_tab), sizeof(long long) * kPendingSlots) &&
+            alloc(reinterpret_cast<void**>(&T.pend_keys), sizeof(long long) * kPendingSlots) &&
+            alloc(reinterpret_cast<void**>(&T.pend_idx), sizeof(int) * kPendingSlots) &&
+            alloc(reinterpret_cast<void**>(&T.alloc), sizeof(AllocState)) &&
+            alloc(reinterpret_cast<void**>(&T.pool), sizeof(double) * kBlockDoubles * cap) &&
+            alloc(reinterpret_cast<void**>(&v->d_ws), sizeof(WinState)) &&
+            alloc(reinterpret_cast<void**>(&v->d_u64), sizeof(unsigned long long) * 8) &&
+            alloc(reinterpret_cast<void**>(&v->d_f64), sizeof(double) * 8) &&
+            cudaMallocHost(&v->h_ws, sizeof(WinState)) == cudaSuccess &&
+            cudaMallocHost(&v->h_u64, sizeof(unsigned long long) * 8) == cudaSuccess &&
+            cudaMallocHost(&v->h_f64, sizeof(double) * 8) == cudaSuccess &&
+            cudaMallocHost(&v->h_alloc, sizeof(AllocState)) == cudaSuccess;
+  if (!ok) {
+    rf_volume_destroy(v);
+    return RF_CAPACITY;
+  }
+  cudaMemset(T.heads, 0xff, sizeof(int) * cfg->hash_buckets);
+  cudaMemset(T.keys, 0xff, sizeof(long long) * cap);
+  cudaMemset(T.pend_tab, 0xff, sizeof(long long) * kPendingSlots);
+  cudaMemset(T.nz, 0, sizeof(int) * cap);
+  cudaMemset(T.stamp, 0, sizeof(unsigned) * cap);
+  cudaMemset(T.alloc, 0, sizeof(AllocState));
+  cudaMemset(v->d_ws, 0, sizeof(WinState));
+  if (ensure_ops(v, 64) != RF_OK || cudaDeviceSynchronize() != cudaSuccess) {
+    rf_volume_destroy(v);
+    return RF_CUDA;
+  }
+  *out = v;
+  return RF_OK;
+}
+
+rf_status rf_volume_destroy(rf_volume* v) {
+  if (!v) return RF_OK;
+  cudaSetDevice(v->cfg.device);
+  cudaDeviceSynchronize();
+  Table& T = v->T;
+  void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched,
+                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  void* hptrs[] = {v->h_ws, v->h_u64, v->h_f64, v->h_alloc, v->h_ops};
+  for (void* p : hptrs)
+    if (p) cudaFreeHost(p);
+  for (auto& e : v->events) {
+    cudaEventDestroy(e.a);
+    cudaEventDestroy(e.b);
+  }
+  for (auto e : v->event_pool) cudaEventDestroy(e);
+  delete v;
+  return RF_OK;
+}
+
+rf_status rf_set_cuda_stream(rf_volume* v, void* stream) {
+  if (!v) return RF_INVALID_ARG;
+  v->stream = static_cast<cudaStream_t>(stream);
+  return RF_OK;
+}
+
+rf_status rf_stream(rf_volume* v, const double center[3], rf_stream_result* result) {
+  if (!v || !center) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  op_stream(b, center);
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  if (result) {
+    result->streamed_in = static_cast<int64_t>(v->h_ops[0].streamed_in);
+    result->streamed_out = static_cast<int64_t>(v->h_ops[0].streamed_out);
+    result->relocated = b.streams[0].relocated;
+  }
+  return RF_OK;
+}
+
+rf_status rf_footprint(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, int64_t* keys_host,
+                       int64_t cap, int64_t* n_out) {
+  if (!v || !valid_kf(kf) || !pose || !n_out) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  const long long npix = static_cast<long long>(kf->width) * kf->height;
+  FootprintParams p = footprint_params(v, b, kf, pose, 0);
+  long long dcap = npix * 4 + 1024;
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    long long* d_keys = nullptr;
+    RF_CUDA_TRY(v, cudaMallocAsync(&d_keys, sizeof(long long) * dcap, v->stream));
+    cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), v->stream);
+    p.dry_keys = d_keys;
+    p.dry_count = v->d_u64;
+    p.dry_cap = dcap;
+    k_footprint<true><<<footprint_grid(v, kf), 256, 0, v->stream>>>(v->T, p);
+    cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                    v->stream);
+    RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+    const long long got = static_cast<long long>(v->h_u64[0]);
+    if (got <= dcap) {
+      std::vector<long long> keys(static_cast<size_t>(got));
+      if (got)
+        cudaMemcpyAsync(keys.data(), d_keys, sizeof(long long) * got, cudaMemcpyDeviceToHost,
+                        v->stream);
+      cudaFreeAsync(d_keys, v->stream);
+      RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+      std::sort(keys.begin(), keys.end());  // np.unique, volume.py:191-193
+      keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+      *n_out = static_cast<int64_t>(keys.size());
+      if (keys_host)
+        std::memcpy(keys_host, keys.data(),
+                    sizeof(long long) * std::min<long long>(cap, static_cast<long long>(keys.size())));
+      return RF_OK;
+    }
+    cudaFreeAsync(d_keys, v->stream);
+    dcap = got + 1024;
+  }
+  return fail(v, RF_CUDA, "footprint scratch sizing failed");
+}
+
+rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
+                      int64_t* new_keys_host, int64_t cap, int64_t* n_new) {
+  if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  op_fuse(b, kf, pose, 2, 0);
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  if (o.err_kind) return status_of(v, o.err_kind, "allocate_blocks");
+  if (n_new) *n_new = static_cast<int64_t>(v->h_ops[0].n_new);
+  return copy_new_keys(v, 0, new_keys_host, cap);
+}
+
+rf_status rf_integrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
+                       rf_op_result* result, int64_t* new_keys_host, int64_t new_cap) {
+  if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  op_fuse(b, kf, pose, 0, 0);
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  if (o.err_kind) return status_of(v, o.err_kind, "integrate");
+  if (result) {
+    result->blocks_touched = static_cast<int64_t>(v->h_ops[0].n_touched);
+    result->voxels_updated = static_cast<int64_t>(v->h_ops[0].voxels_updated);
+    result->n_new = static_cast<int64_t>(v->h_ops[0].n_new);
+  }
+  return copy_new_keys(v, 0, new_keys_host, new_cap);
+}
+
+rf_status rf_deintegrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
+                         rf_op_result* result) {
+  if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  op_fuse(b, kf, pose, 1, 0);
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  if (result) {
+    result->blocks_touched = static_cast<int64_t>(v->h_ops[0].n_touched);
+    result->voxels_updated = static_cast<int64_t>(v->h_ops[0].voxels_updated);
+    result->n_new = static_cast<int64_t>(v->h_ops[0].n_new);
+  }
+  return status_of(v, o.err_kind, "deintegrate");
+}
+
+rf_status rf_correct(rf_volume* v, int32_t m, const rf_kf_view* kfs, const rf_pose* old_poses,
+                     const rf_pose* new_poses, const double* next_center,
+                     rf_window_result* result) {
+  if (!v || m < 0 || (m > 0 && (!kfs || !old_poses || !new_poses))) return RF_INVALID_ARG;
+  if (m > kMaxWindowOps) return fail(v, RF_INVALID_ARG, "window too long");
+  for (int i = 0; i < m; ++i)
+    if (!valid_kf(&kfs[i])) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  rf_window_result r{};
+  r.failed_entry = -1;
+  r.failed_phase = -1;
+  if (m == 0) {  // reintegration.py:161-162
+    rf_status st = RF_OK;
+    if (next_center) st = rf_stream(v, next_center, nullptr);
+    r.status = st;
+    if (result) *result = r;
+    return st;
+  }
+  Batch b;
+  rf_status st = batch_begin(v, b, 4 * m + 4);
+  if (st != RF_OK) return st;
+  // reintegration.py:163-180
+  op_stream(b, old_poses[0].t);
+  for (int i = 0; i < m; ++i) {
+    op_stream(b, old_poses[i].t);
+    op_fuse(b, &kfs[i], &old_poses[i], 1, i);
+  }
+  op_stream(b, new_poses[0].t);
+  for (int i = 0; i < m; ++i) {
+    op_stream(b, new_poses[i].t);
+    op_fuse(b, &kfs[i], &new_poses[i], 0, i);
+  }
+  op_gc(b);
+  if (next_center) op_stream(b, next_center);  // correct_window, :193-194
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  for (int i = 0; i < b.n_ops; ++i) {
+    if (o.err_kind && i > o.err_op) break;
+    const OpInfo& inf = b.infos[i];
+    if (inf.kind == 1 || inf.kind == 2) {
+      r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched);
+      r.n_new += static_cast<int64_t>(v->h_ops[i].n_new);
+      if (inf.kind == 1) r.voxels_updated += static_cast<int64_t>(v->h_ops[i].voxels_updated);
+    } else if (inf.kind == 3) {
+      r.gc_freed = static_cast<int64_t>(v->h_ops[i].n_new);
+    }
+  }
+  if (!o.err_kind) {
+    r.status = RF_OK;
+    r.n_corrected = m;
+    if (result) *result = r;
+    return RF_OK;
+  }
+  const OpInfo& bad = b.infos[o.err_op];
+  r.failed_entry = bad.entry;
+  r.failed_phase = bad.kind == 2 ? 0 : 1;
+  rf_status wst = status_of(v, o.err_kind, bad.kind == 2 ? "deintegrate" : "integrate");
+  if (o.err_kind == kErrInconsistent && bad.kind == 2 && bad.entry > 0) {
+    // reintegration.py:170-174: re-integrate what was already removed
+    const std::string msg = v->err;
+    Batch rb;
+    st = batch_begin(v, rb, 2 * bad.entry);
+    if (st != RF_OK) return st;
+    for (int i = 0; i < bad.entry; ++i) {
+      op_stream(rb, old_poses[i].t);
+      op_fuse(rb, &kfs[i], &old_poses[i], 0, i);
+    }
+    BatchOutcome ro;
+    st = batch_end(rb, ro);
+    if (st != RF_OK) return st;
+    if (ro.err_kind) {
+      wst = status_of(v, ro.err_kind, "integrate (rollback)");
+    } else {
+      v->err = msg;
+    }
+  }
+  r.status = wst;
+  if (result) *result = r;
+  return wst;
+}
+
+rf_status rf_garbage_collect(rf_volume* v, int64_t* freed) {
+  if (!v) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  Batch b;
+  rf_status st = batch_begin(v, b, 1);
+  if (st != RF_OK) return st;
+  op_gc(b);
+  BatchOutcome o;
+  st = batch_end(b, o);
+  if (st != RF_OK) return st;
+  if (freed) *freed = static_cast<int64_t>(v->h_ops[0].n_new);
+  return RF_OK;
+}
+
+rf_status rf_total_weight(rf_volume* v, double* out) {
+  if (!v || !out) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  if (!v->d_wsums) RF_CUDA_TRY(v, cudaMalloc(&v->d_wsums, sizeof(double) * v->T.capacity));
+  k_wsum_blocks<<<v->n_sms * 8, 256, 0, v->stream>>>(v->T, v->d_wsums);
+  k_ordered_sum<<<1, 256, 0, v->stream>>>(v->T, v->d_wsums, v->d_f64);
+  cudaMemcpyAsync(v->h_f64, v->d_f64, sizeof(double), cudaMemcpyDeviceToHost, v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  *out = v->h_f64[0];
+  return RF_OK;
+}
+
+rf_status rf_counters_get(rf_volume* v, rf_counters* out) {
+  if (!v || !out) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), v->stream);
+  if (v->has_center)
+    k_count_active<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, v->center[0], v->center[1],
+                                                        v->center[2],
+                                                        kBlockSide * v->cfg.voxel_size,
+                                                        v->cfg.stream_radius, v->d_u64);
+  cudaMemcpyAsync(v->h_alloc, v->T.alloc, sizeof(AllocState), cudaMemcpyDeviceToHost, v->stream);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                  v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  out->blocks_streamed_in = static_cast<int64_t>(v->h_alloc->total_streamed_in);
+  out->blocks_streamed_out = static_cast<int64_t>(v->h_alloc->total_streamed_out);
+  out->sphere_relocations = v->relocations;
+  out->block_count = v->h_alloc->n_live;
+  out->active_count = v->has_center ? static_cast<int64_t>(v->h_u64[0]) : 0;
+  out->has_center = v->has_center ? 1 : 0;
+  std::memcpy(out->last_center, v->center, sizeof(v->center));
+  return RF_OK;
+}
+
+rf_status rf_export_blocks(rf_volume* v, int64_t* keys_host, double* data_host, int64_t cap,
+                           int64_t* n_out) {
+  if (!v || !n_out) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  int* d_list = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_list, sizeof(int) * v->T.capacity, v->stream));
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), v->stream);
+  k_list_live<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, d_list, v->d_u64);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                  v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  const long long n = static_cast<long long>(v->h_u64[0]);
+  *n_out = n;
+  if (keys_host && data_host && n > 0) {
+    const long long m = std::min<long long>(n, cap);
+    const long long chunk = 16384;  // bound the staging buffer (16k blocks = 335 MB)
+    long long* d_keys = nullptr;
+    double* d_data = nullptr;
+    const long long c = std::min(chunk, m);
+    RF_CUDA_TRY(v, cudaMallocAsync(&d_keys, sizeof(long long) * c, v->stream));
+    RF_CUDA_TRY(v, cudaMallocAsync(&d_data, sizeof(double) * kBlockDoubles * c, v->stream));
+    for (long long off = 0; off < m; off += c) {
+      const long long k = std::min(c, m - off);
+      k_gather<<<static_cast<int>(std::min<long long>(k, v->n_sms * 8)), 256, 0, v->stream>>>(
+          v->T, d_list + off, k, d_keys, d_data);
+      cudaMemcpyAsync(keys_host + off, d_keys, sizeof(long long) * k, cudaMemcpyDeviceToHost,
+                      v->stream);
+      cudaMemcpyAsync(data_host + off * kBlockDoubles, d_data, sizeof(double) * kBlockDoubles * k,
+                      cudaMemcpyDeviceToHost, v->stream);
+    }
+    cudaFreeAsync(d_keys, v->stream);
+    cudaFreeAsync(d_data, v->stream);
+  }
+  cudaFreeAsync(d_list, v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  return RF_OK;
+}
+
+rf_status rf_import_blocks(rf_volume* v, const int64_t* keys_host, const double* data_host,
+                           int64_t n) {
+  if (!v || n < 0 || (n > 0 && (!keys_host || !data_host))) return RF_INVALID_ARG;
+  if (n == 0) return RF_OK;
+  cudaSetDevice(v->cfg.device);
+  const long long chunk = 16384;
+  long long* d_keys = nullptr;
+  double* d_data = nullptr;
+  int* d_ovf = reinterpret_cast<int*>(v->d_u64);
+  const long long c = std::min<long long>(chunk, n);
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_keys, sizeof(long long) * c, v->stream));
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_data, sizeof(double) * kBlockDoubles * c, v->stream));
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), v->stream);
+  for (long long off = 0; off < n; off += c) {
+    const long long k = std::min(c, n - off);
+    cudaMemcpyAsync(d_keys, keys_host + off, sizeof(long long) * k, cudaMemcpyHostToDevice,
+                    v->stream);
+    cudaMemcpyAsync(d_data, data_host + off * kBlockDoubles, sizeof(double) * kBlockDoubles * k,
+                    cudaMemcpyHostToDevice, v->stream);
+    k_import<<<static_cast<int>(std::min<long long>(k, v->n_sms * 8)), 256, 0, v->stream>>>(
+        v->T, d_keys, d_data, k, d_ovf);
+    k_fixup<<<1, 256, 0, v->stream>>>(v->T);
+  }
+  cudaFreeAsync(d_keys, v->stream);
+  cudaFreeAsync(d_data, v->stream);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                  v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  if (v->h_u64[0]) return fail(v, RF_CAPACITY, "import: block pool capacity exhausted");
+  return RF_OK;
+}
+
+rf_status rf_read_blocks(rf_volume* v, const int64_t* keys_host, int64_t n, double* data_host,
+                         int32_t* found_host) {
+  if (!v || n < 0 || (n > 0 && (!keys_host || !data_host))) return RF_INVALID_ARG;
+  if (n == 0) return RF_OK;
+  cudaSetDevice(v->cfg.device);
+  long long* d_keys = nullptr;
+  long long* d_keys_out = nullptr;
+  double* d_data = nullptr;
+  int* d_slots = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_keys, sizeof(long long) * n, v->stream));
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_keys_out, sizeof(long long) * n, v->stream));
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_slots, sizeof(int) * n, v->stream));
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_data, sizeof(double) * kBlockDoubles * n, v->stream));
+  cudaMemcpyAsync(d_keys, keys_host, sizeof(long long) * n, cudaMemcpyHostToDevice, v->stream);
+  k_lookup<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, d_keys, n, d_slots);
+  k_gather<<<static_cast<int>(std::min<long long>(n, v->n_sms * 8)), 256, 0, v->stream>>>(
+      v->T, d_slots, n, d_keys_out, d_data);
+  cudaMemcpyAsync(data_host, d_data, sizeof(double) * kBlockDoubles * n, cudaMemcpyDeviceToHost,
+                  v->stream);
+  std::vector<int> slots(static_cast<size_t>(n));
+  cudaMemcpyAsync(slots.data(), d_slots, sizeof(int) * n, cudaMemcpyDeviceToHost, v->stream);
+  cudaFreeAsync(d_keys, v->stream);
+  cudaFreeAsync(d_keys_out, v->stream);
+  cudaFreeAsync(d_slots, v->stream);
+  cudaFreeAsync(d_data, v->stream);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  if (found_host)
+    for (long long i = 0; i < n; ++i) found_host[i] = slots[static_cast<size_t>(i)] >= 0;
+  return RF_OK;
+}
+
+rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, double oz,
+                        double voxel_size, const double* rot_wc, double tx, double ty, double tz,
+                        double fx, double fy, double cx, double cy, int32_t width, int32_t height,
+                        const double* kf_depth, const double* kf_weight, const double* kf_color,
+                        double mu, double eps_w, int32_t remove, int32_t* count_out) {
+  if (!d || !w || !c || !rot_wc || !kf_depth || !kf_weight || !count_out || width <= 0 ||
+      height <= 0)
+    return RF_INVALID_ARG;
+  const size_t npix = static_cast<size_t>(width) * height;
+  std::vector<double> blk(kBlockDoubles);
+  for (int l = 0; l < kBlockVoxels; ++l) {
+    blk[l] = d[l];
+    blk[kBlockVoxels + l] = w[l];
+    blk[2 * kBlockVoxels + l] = c[3 * l];
+    blk[3 * kBlockVoxels + l] = c[3 * l + 1];
+    blk[4 * kBlockVoxels + l] = c[3 * l + 2];
+  }
+  double *d_blk = nullptr, *d_kd = nullptr, *d_kw = nullptr, *d_kc = nullptr;
+  int* d_cnt = nullptr;
+  bool ok = cudaMalloc(&d_blk, sizeof(double) * kBlockDoubles) == cudaSuccess &&
+            cudaMalloc(&d_kd, sizeof(double) * npix) == cudaSuccess &&
+            cudaMalloc(&d_kw, sizeof(double) * npix) == cudaSuccess &&
+            cudaMalloc(&d_cnt, sizeof(int)) == cudaSuccess &&
+            (!kf_color || cudaMalloc(&d_kc, sizeof(double) * 3 * npix) == cudaSuccess);
+  rf_status st = RF_OK;
+  if (ok) {
+    cudaMemcpy(d_blk, blk.data(), sizeof(double) * kBlockDoubles, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_kd, kf_depth, sizeof(double) * npix, cudaMemcpyHostToDevice);
+    cudaMemcpy(d_kw, kf_weight, sizeof(double) * npix, cudaMemcpyHostToDevice);
+    if (kf_color) cudaMemcpy(d_kc, kf_color, sizeof(double) * 3 * npix, cudaMemcpyHostToDevice);
+    FuseParams p{};
+    p.kf.depth = d_kd;
+    p.kf.weight = d_kw;
+    p.kf.color = d_kc;
+    p.kf.width = width;
+    p.kf.height = height;
+    p.kf.fx = fx;
+    p.kf.fy = fy;
+    p.kf.cx = cx;
+    p.kf.cy = cy;
+    std::memcpy(p.Rwc, rot_wc, sizeof(p.Rwc));
+    p.t[0] = tx;
+    p.t[1] = ty;
+    p.t[2] = tz;
+    p.voxel_size = voxel_size;
+    p.mu = mu;
+    p.eps_w = eps_w;
+    int cnt = 0;
+    if (remove) {
+      k_fuse_single<kCheckRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+      cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
+      if (cnt == 0) {
+        k_fuse_single<kApplyRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+        cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
+      }
+    } else {
+      k_fuse_single<kIntegrate><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+      cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
+      st = RF_CUDA;
+    } else {
+      cudaMemcpy(blk.data(), d_blk, sizeof(double) * kBlockDoubles, cudaMemcpyDeviceToHost);
+      for (int l = 0; l < kBlockVoxels; ++l) {
+        d[l] = blk[l];
+        w[l] = blk[kBlockVoxels + l];
+        c[3 * l] = blk[2 * kBlockVoxels + l];
+        c[3 * l + 1] = blk[3 * kBlockVoxels + l];
+        c[3 * l + 2] = blk[4 * kBlockVoxels + l];
+      }
+      *count_out = cnt;
+    }
+  } else {
+    st = RF_CUDA;
+  }
+  cudaFree(d_blk);
+  cudaFree(d_kd);
+  cudaFree(d_kw);
+  cudaFree(d_kc);
+  cudaFree(d_cnt);
+  return st;
+}
+
+rf_status rf_profile_begin(rf_volume* v) {
+  if (!v) return RF_INVALID_ARG;
+  for (auto& e : v->events) {
+    v->event_pool.push_back(e.a);
+    v->event_pool.push_back(e.b);
+  }
+  v->events.clear();
+  v->prof_voxels = v->prof_pixels = v->prof_blocks = v->prof_launches = 0;
+  v->profiling = true;
+  return RF_OK;
+}
+
+rf_status rf_profile_end(rf_volume* v, rf_profile* out) {
+  if (!v || !out) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  rf_profile p{};
+  for (auto& e : v->events) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    if (e.kind == 0) {
+      p.fuse_launches++;
+      p.fuse_ms += ms;
+    } else if (e.kind == 1) {
+      p.check_launches++;
+      p.check_ms += ms;
+    } else {
+      p.footprint_launches++;
+      p.footprint_ms += ms;
+    }
+    v->event_pool.push_back(e.a);
+    v->event_pool.push_back(e.b);
+  }
+  v->events.clear();
+  p.voxels_updated = v->prof_voxels;
+  p.pixels = v->prof_pixels;
+  p.blocks_touched = v->prof_blocks;
+  p.kernel_launches = v->prof_launches;
+  v->profiling = false;
+  *out = p;
+  return RF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+"""Host-side pose algebra feeding the kernels' scalar arguments.
+
+Mirrors /root/reference/pkg/src/refusion/geometry.py (Pose :41-62,
+transform :101-104, compose :107-109, inverse :112-114, pose_distance
+:160-170, ray_grid :266-275).  The expressions are evaluated with the same
+numpy operations in the same order, so poses composed here are bit-identical
+to the reference's on the same host.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+ORTHONORMAL_TOL = 1e-6
+DEFAULT_DISTANCE_SCALE = np.array([2.0, 2.0, 2.0, 1.0, 1.0, 1.0])
+
+
+@dataclass
+class Intrinsics:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+
+    def __post_init__(self):
+        if self.fx <= 0 or self.fy <= 0:
+            raise ValueError("focal lengths must be positive")
+        if not (0 <= self.cx < self.width and 0 <= self.cy < self.height):
+            raise ValueError("principal point must lie inside the image")
+
+
+@dataclass
+class Pose:
+    """p_world = rotation @ p_cam + translation."""
+
+    rotation: np.ndarray
+    translation: np.ndarray
+
+    def __post_init__(self):
+        self.rotation = np.asarray(self.rotation, dtype=np.float64)
+        self.translation = np.asarray(self.translation, dtype=np.float64).reshape(3)
+        err = np.abs(self.rotation.T @ self.rotation - np.eye(3)).max()
+        if err > ORTHONORMAL_TOL:
+            raise ValueError(f"rotation not orthonormal (err={err:.2e})")
+        if abs(np.linalg.det(self.rotation) - 1.0) > ORTHONORMAL_TOL:
+            raise ValueError("rotation must have determinant +1")
+
+    @classmethod
+    def identity(cls):
+        return cls(np.eye(3), np.zeros(3))
+
+    def copy(self):
+        return Pose(self.rotation.copy(), self.translation.copy())
+
+
+def transform(T, p):
+    p = np.asarray(p, dtype=np.float64)
+    return p @ T.rotation.T + T.translation
+
+
+def compose(T, U):
+    """Apply U first, then T."""
+    return Pose(T.rotation @ U.rotation, T.rotation @ U.translation + T.translation)
+
+
+def inverse(T):
+    r_inv = T.rotation.T
+    return Pose(r_inv, -r_inv @ T.translation)
+
+
+def rotation_x(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[1, 0, 0], [0, c, -s], [0, s, c]], dtype=np.float64)
+
+
+def rotation_y(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, 0, s], [0, 1, 0], [-s, 0, c]], dtype=np.float64)
+
+
+def rotation_z(a):
+    c, s = np.cos(a), np.sin(a)
+    return np.array([[c, -s, 0], [s, c, 0], [0, 0, 1]], dtype=np.float64)
+
+
+def euler_zyx(R):
+    """(yaw, pitch, roll); at the gimbal singularity roll is 0 and the
+    remaining rotation is attributed to yaw (geometry.py:137-157)."""
+    sp = min(1.0, max(-1.0, -R[2, 0]))
+    pitch = np.arcsin(sp)
+    if abs(sp) < 1.0 - 1e-12:
+        yaw = np.arctan2(R[1, 0], R[0, 0])
+        roll = np.arctan2(R[2, 1], R[2, 2])
+    else:
+        yaw = np.arctan2(-R[0, 1], R[1, 1])
+        roll = 0.0
+    return np.array([yaw, pitch, roll], dtype=np.float64)
+
+
+def wrap_angle(a):
+    return np.pi - np.mod(np.pi - np.asarray(a, dtype=np.float64), 2.0 * np.pi)
+
+
+def pose_distance(T, U, s=DEFAULT_DISTANCE_SCALE):
+    """Scaled norm of (wrapped Euler difference, translation difference)."""
+    ea, eb = euler_zyx(T.rotation), euler_zyx(U.rotation)
+    d = np.concatenate([wrap_angle(ea - eb), T.translation - U.translation])
+    return float(np.linalg.norm(np.asarray(s, dtype=np.float64) * d))
+
+
+def rotation_angle(R):
+    cos_a = min(1.0, max(-1.0, (np.trace(R) - 1.0) / 2.0))
+    angle = float(np.arccos(cos_a))
+    return 0.0 if angle < 1e-12 else angle
+
+
+def ray_grid(k):
+    """Unit-depth ray directions ((u-cx)/fx, (v-cy)/fy), each (height, width)."""
+    u = np.arange(k.width, dtype=np.float64)
+    v = np.arange(k.height, dtype=np.float64)
+    dir_x = np.broadcast_to((u - k.cx) / k.fx, (k.height, k.width))
+    dir_y = np.broadcast_to(((v - k.cy) / k.fy)[:, None], (k.height, k.width))
+    return np.ascontiguousarray(dir_x), np.ascontiguousarray(dir_y)

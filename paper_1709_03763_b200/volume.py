@@ -1,0 +1,595 @@
+"""Sparse voxel-hashed TSDF volume resident in B200 HBM.
+
+Drop-in for ``refusion.volume`` (/root/reference/pkg/src/refusion/volume.py):
+the same functions with the same signatures, argument meaning and errors,
+backed by the sm_100a kernels behind include/refusion_b200.h.  What differs
+is where the data lives:
+
+* A ``TwoTierStore`` owns one device volume (hash buckets with linked-list
+  overflow + a pool of 8^3 blocks).  It binds to its ``VolumeConfig`` on the
+  first call that passes one; later calls must pass an equal config.
+* The two tiers of the reference (volume.py:96-123) are a pure function of
+  the streaming centre -- a block is active iff its centre lies within
+  ``stream_radius`` of ``last_center`` -- so no tier state is stored;
+  ``store.active`` / ``store.host`` are computed snapshots.
+* Blocks read back through ``find`` / ``iter_blocks`` / ``active`` are host
+  COPIES; mutating them does not write to the device (use
+  ``store.put_block``).
+* Keyframe planes may be numpy arrays (uploaded per call) or CUDA float64
+  tensors (used in place).
+"""
+
+import ctypes
+import os
+import struct
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+from .errors import CapacityError, StreamingContractError, VolumeInconsistencyError
+
+BLOCK_SIDE = 8
+BLOCK_VOXELS = BLOCK_SIDE ** 3
+EPS_W = 1e-9                      # volume.py:26
+_MIN_SAMPLE_Z_FACTOR = 0.25       # volume.py:30
+_HASH_PRIMES = (73856093, 19349669, 83492791)
+_PACK_BIAS = 1 << 20
+_PACK_SPAN = 1 << 21
+
+DEFAULT_BLOCK_CAPACITY = int(os.environ.get("REFUSION_B200_BLOCKS", str(1 << 16)))
+
+
+@dataclass(frozen=True)
+class VolumeConfig:
+    """volume.py:39-66 -- geometry of the volume and of the streaming sphere."""
+
+    voxel_size: float = 0.01
+    mu: float = 0.06
+    stream_radius: float = 3.0
+    hash_buckets: int = 1 << 16
+
+    def __post_init__(self):
+        if not self.voxel_size > 0.0:
+            raise ValueError(f"voxel_size must be > 0, got {self.voxel_size}")
+        if not self.mu >= 2.0 * self.voxel_size:
+            raise ValueError(
+                f"mu must be at least two voxels ({2.0 * self.voxel_size}), got {self.mu}")
+        if not self.stream_radius > self.mu:
+            raise ValueError(
+                f"stream_radius must exceed mu={self.mu}, got {self.stream_radius}")
+        if self.hash_buckets <= 0:
+            raise ValueError(f"hash_buckets must be > 0, got {self.hash_buckets}")
+
+    @property
+    def block_span(self):
+        return BLOCK_SIDE * self.voxel_size
+
+
+class VoxelBlock:
+    """Host copy of one 8x8x8 brick (flat arrays, x fastest)."""
+
+    __slots__ = ("coord", "d", "w", "c")
+
+    def __init__(self, coord, d=None, w=None, c=None):
+        self.coord = (int(coord[0]), int(coord[1]), int(coord[2]))
+        self.d = np.zeros(BLOCK_VOXELS) if d is None else d
+        self.w = np.zeros(BLOCK_VOXELS) if w is None else w
+        self.c = np.zeros((BLOCK_VOXELS, 3)) if c is None else c
+
+    def copy(self):
+        return VoxelBlock(self.coord, self.d.copy(), self.w.copy(), self.c.copy())
+
+
+@dataclass(frozen=True)
+class IntegrationRecord:
+    """volume.py:126-134"""
+
+    kf: object
+    pose: object
+    new_blocks: frozenset = field(default_factory=frozenset)
+    blocks_touched: int = 0
+    voxels_updated: int = 0
+
+
+def block_hash(coord, buckets):
+    """volume.py:84-93 (pure host arithmetic, Python floor-mod)."""
+    if buckets <= 0:
+        raise ValueError(f"buckets must be > 0, got {buckets}")
+    h = (int(coord[0]) * _HASH_PRIMES[0] ^ int(coord[1]) * _HASH_PRIMES[1]
+         ^ int(coord[2]) * _HASH_PRIMES[2])
+    return h % buckets
+
+
+def pack_keys(coords):
+    a = np.asarray(coords, dtype=np.int64).reshape(-1, 3)
+    return ((a[:, 0] + _PACK_BIAS) << 42) | ((a[:, 1] + _PACK_BIAS) << 21) | (a[:, 2] + _PACK_BIAS)
+
+
+def unpack_keys(keys):
+    keys = np.asarray(keys, dtype=np.int64)
+    kz = keys & (_PACK_SPAN - 1)
+    ky = (keys >> 21) & (_PACK_SPAN - 1)
+    kx = keys >> 42
+    return np.stack([kx - _PACK_BIAS, ky - _PACK_BIAS, kz - _PACK_BIAS], axis=-1)
+
+
+def keys_to_coords(keys):
+    return [tuple(int(x) for x in row) for row in unpack_keys(keys)]
+
+
+# ---------------------------------------------------------------------------
+# argument marshalling
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _check(vol_ptr, status, what):
+    if status == L.RF_OK:
+        return
+    msg = L.lib().rf_last_error(vol_ptr) if vol_ptr else b""
+    msg = (msg or b"").decode() or L.lib().rf_status_string(status).decode()
+    if status == L.RF_STREAMING_CONTRACT:
+        raise StreamingContractError(msg)
+    if status == L.RF_INCONSISTENT:
+        raise VolumeInconsistencyError(msg)
+    if status == L.RF_CAPACITY:
+        raise CapacityError(msg)
+    if status == L.RF_INVALID_ARG:
+        raise ValueError(f"{what}: invalid argument {msg}")
+    raise RuntimeError(f"{what}: {msg}")
+
+
+def pose_struct(pose):
+    p = L.RfPose()
+    R = np.ascontiguousarray(np.asarray(pose.rotation, dtype=np.float64)).reshape(9)
+    t = np.ascontiguousarray(np.asarray(pose.translation, dtype=np.float64)).reshape(3)
+    for i in range(9):
+        p.R[i] = float(R[i])
+    for i in range(3):
+        p.t[i] = float(t[i])
+    return p
+
+
+def _device_plane(arr, shape, device):
+    """CUDA float64 contiguous tensor for a plane (numpy / torch input)."""
+    torch = _torch()
+    if isinstance(arr, torch.Tensor):
+        t = arr
+        if t.dtype != torch.float64:
+            t = t.to(torch.float64)
+        if not t.is_cuda or t.device.index != device:
+            t = t.to(f"cuda:{device}", non_blocking=True)
+        t = t.contiguous()
+    else:
+        a = np.ascontiguousarray(np.asarray(arr, dtype=np.float64))
+        t = torch.from_numpy(a).to(f"cuda:{device}")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"keyframe plane shape {tuple(t.shape)} != {tuple(shape)}")
+    return t
+
+
+def kf_view(kf, device=0):
+    """(rf_kf_view, keep-alive tensors) for a duck-typed keyframe."""
+    intr = kf.intrinsics
+    h, w = int(intr.height), int(intr.width)
+    depth = _device_plane(kf.depth, (h, w), device)
+    weight = _device_plane(kf.weight, (h, w), device)
+    color = getattr(kf, "color", None)
+    color_t = None if color is None else _device_plane(color, (h, w, 3), device)
+    v = L.RfKfView()
+    v.depth = depth.data_ptr()
+    v.weight = weight.data_ptr()
+    v.color = color_t.data_ptr() if color_t is not None else None
+    v.width, v.height = w, h
+    v.fx, v.fy, v.cx, v.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
+    return v, (depth, weight, color_t)
+
+
+# ---------------------------------------------------------------------------
+# the store
+
+
+class TwoTierStore:
+    """Device-resident counterpart of volume.TwoTierStore (volume.py:96-123)."""
+
+    def __init__(self, block_capacity=None, device=None, shard_rank=0, shard_count=1):
+        self.block_capacity = int(block_capacity or DEFAULT_BLOCK_CAPACITY)
+        self.device = device
+        self.shard_rank = int(shard_rank)
+        self.shard_count = int(shard_count)
+        self._ptr = None
+        self._cfg = None
+        self._pending = None  # blocks loaded before the store was bound
+
+    # -- binding ------------------------------------------------------------
+    def _bind(self, cfg):
+        if self._ptr is not None:
+            if cfg is not None and cfg != self._cfg:
+                raise ValueError(f"store is bound to {self._cfg}, got {cfg}")
+            return self._ptr
+        if cfg is None:
+            return None
+        torch = _torch()
+        lib = L.lib()
+        dev = torch.cuda.current_device() if self.device is None else int(self.device)
+        self.device = dev
+        c = L.RfConfig(cfg.voxel_size, cfg.mu, cfg.stream_radius, int(cfg.hash_buckets),
+                       self.block_capacity, dev, self.shard_rank, self.shard_count, 0)
+        ptr = ctypes.c_void_p()
+        with torch.cuda.device(dev):
+            st = lib.rf_volume_create(ctypes.byref(c), ctypes.byref(ptr))
+        if st != L.RF_OK:
+            if st == L.RF_CAPACITY:
+                raise CapacityError(
+                    f"cannot allocate {self.block_capacity} blocks on cuda:{dev}")
+            _check(None, st, "TwoTierStore")
+        self._ptr = ptr
+        self._cfg = cfg
+        if self._pending is not None:
+            keys, data = self._pending
+            self._pending = None
+            self._import(keys, data)
+        return ptr
+
+    @property
+    def bound(self):
+        return self._ptr is not None
+
+    @property
+    def config(self):
+        return self._cfg
+
+    def _call(self, name, *args):
+        torch = _torch()
+        lib = L.lib()
+        with torch.cuda.device(self.device):
+            lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
+            st = getattr(lib, name)(self._ptr, *args)
+        _check(self._ptr, st, name)
+
+    def close(self):
+        if self._ptr is not None:
+            L.lib().rf_volume_destroy(self._ptr)
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+    # -- counters (volume.py:104-110) ---------------------------------------
+    def counters(self):
+        out = L.RfCounters()
+        if self._ptr is None:
+            return out
+        self._call("rf_counters_get", ctypes.byref(out))
+        return out
+
+    @property
+    def blocks_streamed_in(self):
+        return int(self.counters().blocks_streamed_in)
+
+    @property
+    def blocks_streamed_out(self):
+        return int(self.counters().blocks_streamed_out)
+
+    @property
+    def sphere_relocations(self):
+        return int(self.counters().sphere_relocations)
+
+    @property
+    def last_center(self):
+        c = self.counters()
+        return np.array(c.last_center[:], dtype=np.float64) if c.has_center else None
+
+    def block_count(self):
+        if self._ptr is None:
+            return 0 if self._pending is None else len(self._pending[0])
+        return int(self.counters().block_count)
+
+    # -- block access ---------------------------------------------------------
+    def export(self):
+        """(keys int64[n] sorted, d[n,512], w[n,512], c[n,512,3]) host copies."""
+        if self._ptr is None:
+            if self._pending is not None:
+                keys, data = self._pending
+                return _split(np.asarray(keys), np.asarray(data))
+            return (np.zeros(0, np.int64), np.zeros((0, BLOCK_VOXELS)),
+                    np.zeros((0, BLOCK_VOXELS)), np.zeros((0, BLOCK_VOXELS, 3)))
+        n = ctypes.c_int64()
+        self._call("rf_export_blocks", None, None, 0, ctypes.byref(n))
+        cnt = int(n.value)
+        keys = np.zeros(cnt, dtype=np.int64)
+        data = np.zeros((cnt, 5, BLOCK_VOXELS), dtype=np.float64)
+        if cnt:
+            self._call("rf_export_blocks", keys.ctypes.data_as(L.c_int64_p),
+                       data.ctypes.data_as(L.c_double_p), cnt, ctypes.byref(n))
+        order = np.argsort(keys, kind="stable")
+        return _split(keys[order], data[order])
+
+    def _blocks(self):
+        keys, d, w, c = self.export()
+        coords = keys_to_coords(keys)
+        return {coord: VoxelBlock(coord, d[i], w[i], c[i]) for i, coord in enumerate(coords)}
+
+    def find(self, coord):
+        if self._ptr is None:
+            return self._blocks().get(tuple(coord))
+        keys = pack_keys([coord])
+        data = np.zeros((1, 5, BLOCK_VOXELS))
+        found = np.zeros(1, dtype=np.int32)
+        self._call("rf_read_blocks", keys.ctypes.data_as(L.c_int64_p), 1,
+                   data.ctypes.data_as(L.c_double_p), found.ctypes.data_as(L.c_int32_p))
+        if not found[0]:
+            return None
+        _, d, w, c = _split(keys, data)
+        return VoxelBlock(coord, d[0], w[0], c[0])
+
+    def iter_blocks(self):
+        yield from self._blocks().items()
+
+    def _tiers(self):
+        blocks = self._blocks()
+        cfg = self._cfg
+        center = self.last_center
+        if center is None or cfg is None:
+            return {}, blocks
+        coords = list(blocks)
+        if not coords:
+            return {}, {}
+        centers = (np.array(coords, dtype=np.float64) + 0.5) * cfg.block_span
+        inside = np.linalg.norm(centers - center, axis=1) <= cfg.stream_radius
+        active = {c: blocks[c] for c, i in zip(coords, inside) if i}
+        host = {c: blocks[c] for c, i in zip(coords, inside) if not i}
+        return active, host
+
+    @property
+    def active(self):
+        """Snapshot of the blocks inside the streaming sphere."""
+        return self._tiers()[0]
+
+    @property
+    def host(self):
+        """Snapshot of the blocks outside the streaming sphere."""
+        return self._tiers()[1]
+
+    def put_block(self, coord, d=None, w=None, c=None):
+        """Create or overwrite one block's contents on the device."""
+        blk = VoxelBlock(coord, d, w, c)
+        data = np.zeros((1, 5, BLOCK_VOXELS))
+        data[0, 0], data[0, 1] = blk.d, blk.w
+        data[0, 2:] = np.asarray(blk.c).T
+        self._import(pack_keys([coord]), data)
+
+    def _import(self, keys, data):
+        keys = np.ascontiguousarray(keys, dtype=np.int64)
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        if self._ptr is None:
+            if self._pending is None:
+                self._pending = (keys, data)
+            else:
+                self._pending = (np.concatenate([self._pending[0], keys]),
+                                 np.concatenate([self._pending[1], data]))
+            return
+        self._call("rf_import_blocks", keys.ctypes.data_as(L.c_int64_p),
+                   data.ctypes.data_as(L.c_double_p), len(keys))
+
+
+def _split(keys, data):
+    data = np.asarray(data).reshape(-1, 5, BLOCK_VOXELS)
+    d = np.ascontiguousarray(data[:, 0])
+    w = np.ascontiguousarray(data[:, 1])
+    c = np.ascontiguousarray(np.transpose(data[:, 2:], (0, 2, 1)))
+    return np.asarray(keys, dtype=np.int64), d, w, c
+
+
+# ---------------------------------------------------------------------------
+# volume API (volume.py:151-464)
+
+_scratch = {}
+
+
+def _scratch_store(cfg):
+    st = _scratch.get(cfg)
+    if st is None:
+        st = TwoTierStore(block_capacity=1)
+        st._bind(cfg)
+        _scratch[cfg] = st
+    return st
+
+
+def keyframe_block_footprint(kf, pose, cfg):
+    """volume.py:151-197 -- sorted list of the block coords a keyframe can touch."""
+    store = _scratch_store(cfg)
+    view, keep = kf_view(kf, store.device)
+    ps = pose_struct(pose)
+    n = ctypes.c_int64()
+    store._call("rf_footprint", ctypes.byref(view), ctypes.byref(ps), None, 0, ctypes.byref(n))
+    keys = np.zeros(int(n.value), dtype=np.int64)
+    if len(keys):
+        store._call("rf_footprint", ctypes.byref(view), ctypes.byref(ps),
+                    keys.ctypes.data_as(L.c_int64_p), len(keys), ctypes.byref(n))
+    del keep
+    return keys_to_coords(keys)
+
+
+def allocate_blocks(store, kf, pose, cfg):
+    """volume.py:216-220 -- returns the set of newly created coords."""
+    store._bind(cfg)
+    view, keep = kf_view(kf, store.device)
+    ps = pose_struct(pose)
+    cap = max(1, store.block_capacity)
+    new = np.zeros(min(cap, 1 << 22), dtype=np.int64)
+    n = ctypes.c_int64()
+    store._call("rf_allocate", ctypes.byref(view), ctypes.byref(ps),
+                new.ctypes.data_as(L.c_int64_p), len(new), ctypes.byref(n))
+    del keep
+    return set(keys_to_coords(new[: int(n.value)]))
+
+
+def integrate(store, kf, pose, cfg):
+    """volume.py:296-312"""
+    store._bind(cfg)
+    view, keep = kf_view(kf, store.device)
+    ps = pose_struct(pose)
+    res = L.RfOpResult()
+    new = np.zeros(min(max(1, store.block_capacity), 1 << 22), dtype=np.int64)
+    store._call("rf_integrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res),
+                new.ctypes.data_as(L.c_int64_p), len(new))
+    del keep
+    return IntegrationRecord(
+        kf=kf,
+        pose=pose.copy(),
+        new_blocks=frozenset(keys_to_coords(new[: int(res.n_new)])),
+        blocks_touched=int(res.blocks_touched),
+        voxels_updated=int(res.voxels_updated),
+    )
+
+
+def deintegrate(store, kf, pose, cfg):
+    """volume.py:315-338 -- raises VolumeInconsistencyError, volume restored."""
+    store._bind(cfg)
+    view, keep = kf_view(kf, store.device)
+    ps = pose_struct(pose)
+    res = L.RfOpResult()
+    store._call("rf_deintegrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res))
+    del keep
+
+
+def stream(store, center, cfg):
+    """volume.py:351-379 -- counter deltas of one re-centring."""
+    store._bind(cfg)
+    c = np.ascontiguousarray(np.asarray(center, dtype=np.float64).reshape(3))
+    out = L.RfStreamResult()
+    store._call("rf_stream", c.ctypes.data_as(L.c_double_p), ctypes.byref(out))
+    return {"streamed_in": int(out.streamed_in), "streamed_out": int(out.streamed_out),
+            "relocated": int(out.relocated)}
+
+
+def garbage_collect(store):
+    """volume.py:382-390"""
+    if not store.bound:
+        if store._pending is None:
+            return 0
+        keys, data = store._pending
+        live = np.asarray(data)[:, 1].any(axis=1)
+        store._pending = (keys[live], data[live])
+        return int((~live).sum())
+    n = ctypes.c_int64()
+    store._call("rf_garbage_collect", ctypes.byref(n))
+    return int(n.value)
+
+
+def total_weight(store):
+    """volume.py:393-394 (deterministic device reduction)."""
+    if not store.bound:
+        return float(store.export()[2].sum())
+    out = ctypes.c_double()
+    store._call("rf_total_weight", ctypes.byref(out))
+    return float(out.value)
+
+
+def correct_entries(store, entries, cfg, next_center=None):
+    """Batched reintegration._correct_entries (reintegration.py:156-181) plus
+    the optional stream(next_center) of correct_window: one native call, one
+    host synchronisation.  Advances entry.integrated_pose on success."""
+    if not entries:
+        if next_center is not None:
+            stream(store, next_center, cfg)
+        return 0
+    store._bind(cfg)
+    m = len(entries)
+    views = (L.RfKfView * m)()
+    olds = (L.RfPose * m)()
+    news = (L.RfPose * m)()
+    keep = []
+    for i, e in enumerate(entries):
+        v, k = kf_view(e.kf, store.device)
+        views[i] = v
+        keep.append(k)
+        olds[i] = pose_struct(e.integrated_pose)
+        news[i] = pose_struct(e.target_pose)
+    nc = None
+    if next_center is not None:
+        nca = np.ascontiguousarray(np.asarray(next_center, dtype=np.float64).reshape(3))
+        nc = nca.ctypes.data_as(L.c_double_p)
+    res = L.RfWindowResult()
+    try:
+        store._call("rf_correct", m, views, olds, news, nc, ctypes.byref(res))
+    except StreamingContractError:
+        # reference order: entries integrated before the failing one were
+        # already advanced (reintegration.py:176-179)
+        if res.failed_phase == 1:
+            for e in entries[: res.failed_entry]:
+                e.integrated_pose = e.target_pose.copy()
+        raise
+    finally:
+        del keep
+    for e in entries:
+        e.integrated_pose = e.target_pose.copy()
+    return m
+
+
+# ---------------------------------------------------------------------------
+# snapshots (volume.py:397-464)
+
+_MAGIC = b"SDFV1"
+
+
+def save_volume(store, path, cfg):
+    keys, d, w, c = store.export()
+    coords = unpack_keys(keys)
+    with open(path, "wb") as fh:
+        fh.write(_MAGIC)
+        fh.write(struct.pack("<ddq", cfg.voxel_size, cfg.mu, len(keys)))
+        for i in range(len(keys)):
+            fh.write(struct.pack("<iii", *(int(x) for x in coords[i])))
+            rec = np.empty((BLOCK_VOXELS, 5))
+            rec[:, 0] = d[i]
+            rec[:, 1] = w[i]
+            rec[:, 2:] = c[i]
+            fh.write(rec.astype("<f8").tobytes())
+
+
+def load_volume(path, block_capacity=None, device=None):
+    """Returns (store, voxel_size, mu); blocks are uploaded when the store is
+    first bound (the first call passing a VolumeConfig)."""
+    with open(path, "rb") as fh:
+        magic = fh.read(5)
+        if magic != _MAGIC:
+            raise ValueError(f"not a volume snapshot: bad magic {magic!r}")
+        voxel_size, mu, count = struct.unpack("<ddq", fh.read(24))
+        coords = np.zeros((count, 3), dtype=np.int64)
+        data = np.zeros((count, 5, BLOCK_VOXELS))
+        for i in range(count):
+            coords[i] = struct.unpack("<iii", fh.read(12))
+            rec = np.frombuffer(fh.read(BLOCK_VOXELS * 5 * 8), dtype="<f8").reshape(BLOCK_VOXELS, 5)
+            data[i] = rec.T
+    store = TwoTierStore(block_capacity=block_capacity or max(count, DEFAULT_BLOCK_CAPACITY),
+                         device=device)
+    if count:
+        store._pending = (pack_keys(coords), data)
+    return store, voxel_size, mu
+
+
+def compare_volumes(a, b):
+    """volume.py:445-464 -- (max |dD|, max |dC|, max |dW|) over the union."""
+    blocks_a = dict(a.iter_blocks())
+    blocks_b = dict(b.iter_blocks())
+    zero = VoxelBlock((0, 0, 0))
+    dd = dc = dw = 0.0
+    for coord in set(blocks_a) | set(blocks_b):
+        ba = blocks_a.get(coord) or zero
+        bb = blocks_b.get(coord) or zero
+        dw = max(dw, float(np.abs(ba.w - bb.w).max()))
+        both = (ba.w > 0.0) & (bb.w > 0.0)
+        if both.any():
+            dd = max(dd, float(np.abs(ba.d[both] - bb.d[both]).max()))
+            dc = max(dc, float(np.abs(ba.c[both] - bb.c[both]).max()))
+    return dd, dc, dw
