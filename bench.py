@@ -1,0 +1,508 @@
+#!/usr/bin/env python
+"""Benchmark: keyframes re-integrated per second (640x480, 5 mm voxels) and
+ms per pose-graph correction -- BASELINE.json's metric on configs[1]:
+
+  synthetic corridor, 2000 frames -> 400 keyframes (kappa 5), 5 mm voxels,
+  a pose update every 10 keyframes, top-k (m = 10) changed-keyframe
+  re-integration (reintegration.select_topk + correct_topk).
+
+A step = one pose-graph correction: apply one anchor-correction event, pick
+the m most-moved ledger entries, de-integrate each at its old pose and
+re-integrate it at its new pose (the reference's _correct_entries per pick).
+The 400-keyframe volume is built untimed; keyframes live in HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+`--impl reference` times the reference's own CPU implementation (compiled
+into oracle/_ref by oracle/build_ref.sh) on the same workload, on the host.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+H, W = 480, 640
+KAPPA = 5
+N_FRAMES = 2000
+M_TOPK = 10
+EVENT_EVERY_KF = 10
+VOXEL = 0.005
+MU = 0.06
+RADIUS = 7.0   # frustum corners at z_max 5 m lie ~6.3 m from the camera
+DRIFT_T, DRIFT_R = 0.0004, 0.00015      # per keyframe
+WORKLOAD = ("C2 synthetic corridor: 2000 frames -> 400 keyframes (kappa 5), 640x480, "
+            "5 mm voxels, mu 0.06, anchor every 10 KF, one pose update per step, "
+            "top-k m=10 re-integration")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--keyframes", type=int, default=N_FRAMES // KAPPA)
+    ap.add_argument("--m", type=int, default=M_TOPK)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[4:8]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# workload (shared by both arms: same scene, trajectory, drift and events)
+
+
+def kf_poses(n_kf):
+    from paper_1709_03763_b200 import synth as SY
+
+    gt = SY.corridor_trajectory(n_kf * KAPPA)
+    gt_kf = [gt[i * KAPPA] for i in range(n_kf)]
+    drifted = SY.drift_poses(gt_kf, DRIFT_T, DRIFT_R, seed=1)
+    return gt_kf, drifted
+
+
+def make_events(n_anchors, n_events, seed=11):
+    """Event s moves a random subset of anchors 30% of the way back toward
+    their true pose -- a pose-graph backend publishing corrections."""
+    import numpy as np
+
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n_events):
+        k = max(1, n_anchors // 4)
+        out.append(sorted(int(a) for a in rng.choice(n_anchors, size=k, replace=False)))
+    return out
+
+
+class Scenario:
+    """Ledger + anchors over the keyframes (mirrors pipeline.py's anchor
+    bookkeeping: one anchor per EVENT_EVERY_KF keyframes)."""
+
+    def __init__(self, R, G, SY, gt_kf, drifted, keyframes, events):
+        self.R, self.G, self.SY = R, G, SY
+        self.ledger = R.IntegrationLedger()
+        self.true_anchor, self.believed = {}, {}
+        for k, kf in enumerate(keyframes):
+            a = k // EVENT_EVERY_KF
+            if a not in self.believed:
+                self.true_anchor[a] = gt_kf[k]
+                self.believed[a] = drifted[k]
+                self.ledger.declare_anchor(a, drifted[k])
+            rel = G.compose(G.inverse(self.believed[a]), drifted[k])
+            self.ledger.add(kf, k + 1, a, rel, drifted[k])
+        self.events = events
+        self.frac = 0.3
+
+    def event(self, s):
+        upd = {}
+        for a in self.events[s % len(self.events)]:
+            self.believed[a] = self.SY.pose_interpolate(self.believed[a], self.true_anchor[a],
+                                                        self.frac)
+            upd[a] = self.believed[a].copy()
+        return self.R.PoseUpdateEvent(at_frame=s + 1, anchor_poses=upd)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+
+
+def run_b200(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_03763_b200 import _lib as L
+    from paper_1709_03763_b200 import geometry as G
+    from paper_1709_03763_b200 import reintegration as R
+    from paper_1709_03763_b200 import synth as SY
+    from paper_1709_03763_b200 import volume as V
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = torch.device(f"cuda:{local}")
+
+    n_kf = args.keyframes
+    gt_kf, drifted = kf_poses(n_kf)
+    # keyframes: rendered at ground truth on rank 0, broadcast to every shard
+    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=local)
+    keyframes = []
+    for k in range(n_kf):
+        if rank == 0:
+            kf = SY.render_keyframe(rend, gt_kf[k], seed=1000 + k, kappa=KAPPA)
+        else:
+            kf = SY.DeviceKeyframe(SY.DEFAULT_INTRINSICS, gt_kf[k],
+                                   torch.empty((H, W), dtype=torch.float64, device=dev),
+                                   torch.empty((H, W), dtype=torch.float64, device=dev),
+                                   torch.empty((H, W, 3), dtype=torch.float64, device=dev))
+        if world > 1:
+            for t in (kf.depth, kf.weight, kf.color):
+                dist.broadcast(t, src=0)
+        kf.pose = drifted[k]
+        keyframes.append(kf)
+    torch.cuda.synchronize()
+
+    cfg = V.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS, hash_buckets=1 << 21)
+    cap = int(os.environ.get("RF_BENCH_BLOCKS", str(2_600_000 // world + 200_000)))
+    store = V.TwoTierStore(block_capacity=cap, shard_rank=rank, shard_count=world)
+    n_events = args.warmup + 2 * args.steps + 2
+    scen = Scenario(R, G, SY, gt_kf, drifted, keyframes,
+                    make_events((n_kf + EVENT_EVERY_KF - 1) // EVENT_EVERY_KF, n_events))
+    t0 = time.time()
+    for kf, pose in zip(keyframes, drifted):   # pipeline.close_keyframe, untimed
+        V.stream(store, pose.translation, cfg)
+        V.integrate(store, kf, pose, cfg)
+    torch.cuda.synchronize()
+    build_s = time.time() - t0
+    n_blocks = store.block_count()
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MiB > L2
+    lib, vol = L.lib(), store._ptr
+    step_idx = [0]
+
+    def one_step():
+        ev = scen.event(step_idx[0])
+        step_idx[0] += 1
+        R.apply_pose_update(scen.ledger, ev)
+        picks = R.select_topk(scen.ledger, args.m)
+        nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation
+        return R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    times = []
+    corrected = 0
+    lib.rf_profile_begin(vol)
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            corrected += one_step()
+            b.record(stream)
+            b.synchronize()
+            times.append(a.elapsed_time(b))
+    prof = L.RfProfile()
+    lib.rf_profile_end(vol, L.ctypes.byref(prof))
+    torch.cuda.synchronize()
+    total_ms = sum(times)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    kf_per_s = corrected / (total_ms / 1e3)
+
+    # ---- e2e: same steps through the public API with HOST keyframes ------
+    e2e = None
+    if not args.no_e2e:
+        host = {id(kf): kf.to_host(pinned=True) for kf in keyframes}
+        for e in scen.ledger.entries:
+            e.kf = host[id(e.kf)]
+        h2d = 0
+        etimes = []
+        e_corr = 0
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            ev = scen.event(step_idx[0])
+            step_idx[0] += 1
+            R.apply_pose_update(scen.ledger, ev)
+            picks = R.select_topk(scen.ledger, args.m)
+            nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation
+            e_corr += R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+            torch.cuda.synchronize()
+            etimes.append(time.perf_counter() - t1)
+            h2d += len(picks) * H * W * (8 + 8 + 24)
+        e_total = sum(etimes)
+        if world > 1:
+            t = torch.tensor([e_total], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_total = float(t.item())
+        e2e = {"value": e_corr / e_total, "unit": "keyframes/s",
+               "ms_per_correction": 1e3 * e_total / args.steps,
+               "h2d_bytes_per_step": h2d // args.steps,
+               # per pick: the window result read back (rf_window_result + op records)
+               "d2h_bytes_per_step": args.m * (64 + 8 * 88),
+               "path": "reintegration.correct_topk with numpy-free pinned host keyframes "
+                       "(planes uploaded every correction)"}
+
+    # ---- roofline of the dominant kernel (integrate / de-integrate apply) ----
+    peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else {}
+    peak = peaks.get("hbm_gbs")
+    peak_src = "measured" if peak else "fallback"
+    peak = peak or 6650.0
+    alg_bytes = 80.0 * prof.voxels_updated + 40.0 * prof.pixels
+    achieved = alg_bytes / (prof.fuse_ms / 1e3) / 1e9 if prof.fuse_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(REPO, "profiles", "fuse_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("bytes_per_launch")
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
+            "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic, "kernel": "k_fuse<kIntegrate|kApplyRemove>",
+            "launches": int(prof.fuse_launches),
+            "avg_launch_us": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1),
+            "alg_bytes_per_launch": alg_bytes / max(prof.fuse_launches, 1),
+            "bytes_model": "80 B x voxels_updated + 40 B x H*W per launch",
+            "fuse_ms_share": prof.fuse_ms / total_ms if total_ms else None,
+            "check_ms_share": prof.check_ms / total_ms if total_ms else None,
+            "footprint_ms_share": prof.footprint_ms / total_ms if total_ms else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_from(keyframes[:3], drifted[:3], gt_kf[:3])
+
+    out = {
+        "metric": "keyframes re-integrated/sec (640x480, 5 mm voxels) and ms per pose-graph "
+                  "correction",
+        "value": kf_per_s,
+        "unit": "keyframes/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "ms_per_correction": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (GPU sphere-traced analytic corridor, sigma0 z^2 depth noise)",
+        "config": {"workload": WORKLOAD, "keyframes": n_kf, "m": args.m,
+                   "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS,
+                   "hash_buckets": cfg.hash_buckets, "blocks_resident": n_blocks,
+                   "block_capacity": cap, "volume_build_s": round(build_s, 2),
+                   "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+                   "l2": "flushed between steps (256 MiB write, outside the step events)"},
+        "gpu_launches": int(prof.kernel_launches),
+        "roofline": roof,
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    store.close()
+
+
+# ---------------------------------------------------------------------------
+# reference arm (CPU, the unmodified reference compiled into oracle/_ref)
+
+
+def _import_reference():
+    ref = os.path.join(REPO, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "refusion")):
+        raise RuntimeError("oracle/_ref missing: run oracle/build_ref.sh in the build container")
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    os.environ.setdefault("REFUSION_BACKEND", "compiled")
+    from refusion import geometry as RG
+    from refusion import reintegration as RR
+    from refusion import volume as RV
+    from refusion import kernels as RK
+
+    assert RK.BACKEND == "compiled"
+    return RG, RR, RV
+
+
+def _ref_pose(RG, p):
+    return RG.Pose(p.rotation, p.translation)
+
+
+class _HostKF:
+    def __init__(self, depth, weight, color, intr):
+        self.depth, self.weight, self.color, self.intrinsics = depth, weight, color, intr
+
+
+def _reference_store(RG, RV, kfs_np, drifted, cfg):
+    store = RV.TwoTierStore()
+    for kf, p in zip(kfs_np, drifted):
+        RV.stream(store, p.translation, cfg)
+        RV.integrate(store, kf, _ref_pose(RG, p), cfg)
+    return store
+
+
+def cpu_baseline_from(keyframes, drifted, gt_kf):
+    """Reference CPU path on a bounded sample of the same workload: a volume
+    built from 3 of the SAME keyframes (host copies), then 2 single-entry
+    corrections (correct_topk) timed with perf_counter."""
+    RG, RR, RV = _import_reference()
+    intr = RG.Intrinsics(525.0, 525.0, 319.5, 239.5, W, H)
+    kfs = [_HostKF(k.depth.cpu().numpy(), k.weight.cpu().numpy(), k.color.cpu().numpy(), intr)
+           for k in keyframes]
+    cfg = RV.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS)
+    store = _reference_store(RG, RV, kfs, drifted, cfg)
+    return _time_reference_corrections(RG, RR, RV, store, kfs, drifted, gt_kf, cfg, n=2)
+
+
+def _time_reference_corrections(RG, RR, RV, store, kfs, drifted, gt_kf, cfg, n):
+    ledger = RR.IntegrationLedger()
+    ledger.declare_anchor(0, RG.Pose.identity())
+    for i, (kf, p) in enumerate(zip(kfs, drifted)):
+        ledger.add(kf, i + 1, 0, _ref_pose(RG, p), _ref_pose(RG, p))
+    for i, e in enumerate(ledger.entries):  # corrected target: back to ground truth
+        e.target_pose = _ref_pose(RG, gt_kf[i])
+    picks = RR.select_topk(ledger, n)
+    t0 = time.perf_counter()
+    done = RR.correct_topk(store, ledger, picks, cfg,
+                           next_center=ledger.entries[picks[0] - 1].target_pose.translation)
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "keyframes/s", "cores": 1,
+            "threads_available": os.cpu_count(), "kind": "reference",
+            "ms_per_correction_of_1_kf": 1e3 * dt / done,
+            "sample": f"{done} single-keyframe corrections (correct_topk) at 640x480, 5 mm, "
+                      f"volume of {len(kfs)} corridor keyframes; reference is single-threaded "
+                      f"Python + Cython (BLAS may use all cores)"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    RG, RR, RV = _import_reference()
+    from refusion import synth as RS
+
+    from paper_1709_03763_b200 import synth as SY  # host-only pose helpers / scene spec
+
+    n_kf = 3
+    gt_kf, drifted = kf_poses(args.keyframes)
+    gt_kf, drifted = gt_kf[:n_kf], drifted[:n_kf]
+    prims = []
+    for p in SY.corridor_scene():
+        if p.kind == SY.ROOM:
+            prims.append(RS.RoomShell(p.center, p.size, p.albedo))
+        elif p.kind == SY.BOX:
+            prims.append(RS.BoxSolid(p.center, p.size, p.albedo))
+        else:
+            prims.append(RS.Sphere(p.center, p.size[0], p.albedo))
+    scene = RS.AnalyticScene(prims)
+    intr = RS.DEFAULT_INTRINSICS
+    kfs = []
+    for k in range(n_kf):
+        gp = _ref_pose(RG, gt_kf[k])
+        depth = RS.add_noise(RS.render_depth(scene, gp, intr, z_max=5.0), seed=(1, 7, k),
+                             sigma0=0.0015)
+        color = RS.render_color(scene, gp, intr, depth)
+        weight = np.where(depth > 0, KAPPA / np.maximum(depth * depth, 1e-12), 0.0)
+        kfs.append(_HostKF(depth, weight, color, intr))
+    cfg = RV.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS)
+    store = _reference_store(RG, RV, kfs, drifted, cfg)
+    times = []
+    for s in range(args.warmup + args.steps):
+        # each step: one correction re-integrating one keyframe (bounded sample)
+        i = s % n_kf
+        ledger = RR.IntegrationLedger()
+        ledger.declare_anchor(0, RG.Pose.identity())
+        e = ledger.add(kfs[i], i + 1, 0, _ref_pose(RG, drifted[i]), _ref_pose(RG, drifted[i]))
+        target = SY.pose_interpolate(drifted[i], gt_kf[i], 0.3 + 0.05 * (s % 5))
+        e.target_pose = _ref_pose(RG, target)
+        t0 = time.perf_counter()
+        RR.correct_topk(store, ledger, [1], cfg, next_center=e.target_pose.translation)
+        dt = time.perf_counter() - t0
+        drifted[i] = target
+        if s >= args.warmup:
+            times.append(dt)
+    total = sum(times)
+    value = len(times) / total
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "keyframes re-integrated/sec (640x480, 5 mm voxels) and ms per pose-graph "
+                  "correction",
+        "value": value, "unit": "keyframes/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference synth.py renderer, same corridor scene and poses)",
+        "config": {"workload": WORKLOAD, "sample": "each step = one single-keyframe "
+                   "correction (correct_topk, m=1) on a 3-keyframe corridor volume",
+                   "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS},
+        "cpu_baseline": {"value": value, "unit": "keyframes/s", "cores": 1,
+                         "threads_available": os.cpu_count(), "kind": "reference",
+                         "sample": "single-keyframe corrections, 640x480, 5 mm"},
+        "e2e": {"value": value, "unit": "keyframes/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

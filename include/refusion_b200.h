@@ -101,7 +101,7 @@ typedef struct rf_window_result {
     int32_t status;          /* rf_status of the window */
     int32_t failed_entry;    /* entry index that raised, -1 if none */
     int32_t failed_phase;    /* 0 de-integration, 1 integration, -1 none */
-    int32_t _pad;
+    int32_t failed_window;   /* window index that raised (rf_correct_windows), -1 if none */
     int64_t n_corrected;     /* entries re-integrated (0 on error) */
     int64_t voxels_updated;  /* summed over the integrate phase */
     int64_t blocks_touched;  /* summed over all (de)integrations */
@@ -161,6 +161,15 @@ rf_status rf_deintegrate(rf_volume *vol, const rf_kf_view *kf, const rf_pose *po
 rf_status rf_correct(rf_volume *vol, int32_t m, const rf_kf_view *kfs,
                      const rf_pose *old_poses, const rf_pose *new_poses,
                      const double *next_center, rf_window_result *result);
+/* n_windows back-to-back _correct_entries calls (correct_topk's one window
+ * per pick, finalize's runs of m) in one batch with ONE host sync: window w
+ * holds sizes[w] consecutive entries of kfs / old_poses / new_poses.  On an
+ * error the windows before the failing one stay applied (as sequential
+ * calls would leave them) and result->failed_window names it. */
+rf_status rf_correct_windows(rf_volume *vol, int32_t n_windows, const int32_t *sizes,
+                             const rf_kf_view *kfs, const rf_pose *old_poses,
+                             const rf_pose *new_poses, const double *next_center,
+                             rf_window_result *result);
 /* garbage_collect (volume.py:382-390) */
 rf_status rf_garbage_collect(rf_volume *vol, int64_t *freed);
 /* total_weight (volume.py:393-394) */

@@ -90,7 +90,7 @@ class RfWindowResult(ctypes.Structure):
         ("status", ctypes.c_int32),
         ("failed_entry", ctypes.c_int32),
         ("failed_phase", ctypes.c_int32),
-        ("_pad", ctypes.c_int32),
+        ("failed_window", ctypes.c_int32),
         ("n_corrected", ctypes.c_int64),
         ("voxels_updated", ctypes.c_int64),
         ("blocks_touched", ctypes.c_int64),
@@ -161,6 +161,9 @@ SIGNATURES = {
                             ctypes.POINTER(RfOpResult)]),
     "rf_correct": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
                         ctypes.POINTER(RfPose), c_double_p, ctypes.POINTER(RfWindowResult)]),
+    "rf_correct_windows": (_S, [_vp, ctypes.c_int32, c_int32_p, ctypes.POINTER(RfKfView),
+                                ctypes.POINTER(RfPose), ctypes.POINTER(RfPose), c_double_p,
+                                ctypes.POINTER(RfWindowResult)]),
     "rf_garbage_collect": (_S, [_vp, c_int64_p]),
     "rf_total_weight": (_S, [_vp, c_double_p]),
     "rf_counters_get": (_S, [_vp, ctypes.POINTER(RfCounters)]),

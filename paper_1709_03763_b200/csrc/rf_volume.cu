@@ -58,6 +58,7 @@ struct rf_volume {
   unsigned epoch = 0;
   int n_sms = 148;
   int fuse_grid = 148 * 2;
+  int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
   int fp_grid_cap = 148 * 8;
   // profiling
   bool profiling = false;
@@ -140,6 +141,7 @@ struct PendingStream {
 struct OpInfo {
   int kind;  // 0 stream, 1 integrate, 2 deintegrate, 3 gc, 4 allocate
   int entry;
+  int window = 0;
 };
 
 struct Batch {
@@ -149,6 +151,7 @@ struct Batch {
   double center[3];
   std::vector<PendingStream> streams;
   std::vector<OpInfo> infos;
+  std::vector<FuseParams> fparams;  // per op (fuse ops only)
   int gc_op = -1;
 };
 
@@ -179,6 +182,7 @@ void op_stream(Batch& b, const double c[3]) {
   rf_volume* v = b.v;
   const int op = b.n_ops++;
   b.infos.push_back({0, -1});
+  b.fparams.emplace_back();
   StreamParams p{};
   std::memcpy(p.old_c, b.center, sizeof(p.old_c));
   std::memcpy(p.new_c, c, sizeof(p.new_c));
@@ -261,6 +265,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     k_commit<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
   }
   FuseParams p = fuse_params(v, kf, pose, op);
+  b.fparams.push_back(p);
   if (mode == 2) {
     p.alloc_only = 1;
     k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
@@ -272,10 +277,10 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   } else {
     {
       ProfScope ps(v, 1);
-      k_fuse<kCheckRemove><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+      k_fuse<kCheckRemove><<<v->fuse_grids[kCheckRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
     }
     ProfScope ps(v, 0);
-    k_fuse<kApplyRemove><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    k_fuse<kApplyRemove><<<v->fuse_grids[kApplyRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
   }
   if (v->profiling) {
     v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
@@ -287,6 +292,7 @@ void op_gc(Batch& b) {
   rf_volume* v = b.v;
   const int op = b.n_ops++;
   b.infos.push_back({3, -1});
+  b.fparams.emplace_back();
   b.gc_op = op;
   const long long grid = std::min<long long>((v->cfg.hash_buckets + 255) / 256, v->n_sms * 8);
   // freed count lands in the op's n_new field
@@ -311,6 +317,14 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
   RF_CUDA_TRY(v, cudaGetLastError());
   out.err_kind = v->h_ws->err_kind;
   out.err_op = out.err_kind ? v->h_ws->err_op : -1;
+  if (out.err_kind == kErrInconsistent) {
+    // volume.py:331-333: blocks sorted before the failing one were removed
+    // and re-added; the rest stays untouched.  The later ops were skipped,
+    // so the failed op's touched list is still intact.
+    k_fuse<kRemoveReadd><<<v->fuse_grids[kRemoveReadd], kFuseThreads, 0, v->stream>>>(v->T, b.fparams[out.err_op]);
+    RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+    RF_CUDA_TRY(v, cudaGetLastError());
+  }
   for (const PendingStream& s : b.streams) {
     if (out.err_kind && s.op > out.err_op) break;
     v->has_center = true;
@@ -406,9 +420,13 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
     return RF_CUDA;
   }
   cudaDeviceGetAttribute(&v->n_sms, cudaDevAttrMultiProcessorCount, cfg->device);
-  int occ = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_fuse<kIntegrate>, kFuseThreads, 0);
-  v->fuse_grid = v->n_sms * std::max(occ, 1);
+  int occ[4] = {1, 1, 1, 1};
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, 0);
+  for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
+  v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
   const size_t cap = static_cast<size_t>(cfg->block_capacity);
   Table& T = v->T;
@@ -599,73 +617,92 @@ rf_status rf_deintegrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose
   return status_of(v, o.err_kind, "deintegrate");
 }
 
-rf_status rf_correct(rf_volume* v, int32_t m, const rf_kf_view* kfs, const rf_pose* old_poses,
-                     const rf_pose* new_poses, const double* next_center,
-                     rf_window_result* result) {
-  if (!v || m < 0 || (m > 0 && (!kfs || !old_poses || !new_poses))) return RF_INVALID_ARG;
-  if (m > kMaxWindowOps) return fail(v, RF_INVALID_ARG, "window too long");
-  for (int i = 0; i < m; ++i)
+rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* sizes,
+                             const rf_kf_view* kfs, const rf_pose* old_poses,
+                             const rf_pose* new_poses, const double* next_center,
+                             rf_window_result* result) {
+  if (!v || n_windows < 0 || (n_windows > 0 && !sizes)) return RF_INVALID_ARG;
+  long long total = 0;
+  for (int w = 0; w < n_windows; ++w) {
+    if (sizes[w] < 0) return RF_INVALID_ARG;
+    total += sizes[w];
+  }
+  if (total > kMaxWindowOps) return fail(v, RF_INVALID_ARG, "too many entries in one call");
+  if (total > 0 && (!kfs || !old_poses || !new_poses)) return RF_INVALID_ARG;
+  for (long long i = 0; i < total; ++i)
     if (!valid_kf(&kfs[i])) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
   rf_window_result r{};
   r.failed_entry = -1;
   r.failed_phase = -1;
-  if (m == 0) {  // reintegration.py:161-162
-    rf_status st = RF_OK;
-    if (next_center) st = rf_stream(v, next_center, nullptr);
-    r.status = st;
-    if (result) *result = r;
-    return st;
-  }
+  r.failed_window = -1;
   Batch b;
-  rf_status st = batch_begin(v, b, 4 * m + 4);
+  rf_status st = batch_begin(v, b, static_cast<int>(4 * total + 2 * n_windows + 2));
   if (st != RF_OK) return st;
-  // reintegration.py:163-180
-  op_stream(b, old_poses[0].t);
-  for (int i = 0; i < m; ++i) {
-    op_stream(b, old_poses[i].t);
-    op_fuse(b, &kfs[i], &old_poses[i], 1, i);
+  // each window is reintegration._correct_entries (reintegration.py:156-181)
+  long long base = 0;
+  for (int w = 0; w < n_windows; ++w) {
+    const int m = sizes[w];
+    if (m == 0) continue;  // :161-162
+    const rf_kf_view* k = kfs + base;
+    const rf_pose* o = old_poses + base;
+    const rf_pose* n = new_poses + base;
+    op_stream(b, o[0].t);
+    for (int i = 0; i < m; ++i) {
+      op_stream(b, o[i].t);
+      op_fuse(b, &k[i], &o[i], 1, i);
+      b.infos.back().window = w;
+    }
+    op_stream(b, n[0].t);
+    for (int i = 0; i < m; ++i) {
+      op_stream(b, n[i].t);
+      op_fuse(b, &k[i], &n[i], 0, i);
+      b.infos.back().window = w;
+    }
+    op_gc(b);
+    b.infos.back().window = w;
+    base += m;
   }
-  op_stream(b, new_poses[0].t);
-  for (int i = 0; i < m; ++i) {
-    op_stream(b, new_poses[i].t);
-    op_fuse(b, &kfs[i], &new_poses[i], 0, i);
-  }
-  op_gc(b);
-  if (next_center) op_stream(b, next_center);  // correct_window, :193-194
-  BatchOutcome o;
-  st = batch_end(b, o);
+  if (next_center) op_stream(b, next_center);  // correct_window / correct_topk
+  BatchOutcome out;
+  st = batch_end(b, out);
   if (st != RF_OK) return st;
   for (int i = 0; i < b.n_ops; ++i) {
-    if (o.err_kind && i > o.err_op) break;
+    if (out.err_kind && i > out.err_op) break;
     const OpInfo& inf = b.infos[i];
     if (inf.kind == 1 || inf.kind == 2) {
       r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched);
       r.n_new += static_cast<int64_t>(v->h_ops[i].n_new);
       if (inf.kind == 1) r.voxels_updated += static_cast<int64_t>(v->h_ops[i].voxels_updated);
     } else if (inf.kind == 3) {
-      r.gc_freed = static_cast<int64_t>(v->h_ops[i].n_new);
+      r.gc_freed += static_cast<int64_t>(v->h_ops[i].n_new);
     }
   }
-  if (!o.err_kind) {
+  if (!out.err_kind) {
     r.status = RF_OK;
-    r.n_corrected = m;
+    r.n_corrected = total;
     if (result) *result = r;
     return RF_OK;
   }
-  const OpInfo& bad = b.infos[o.err_op];
+  const OpInfo& bad = b.infos[out.err_op];
   r.failed_entry = bad.entry;
   r.failed_phase = bad.kind == 2 ? 0 : 1;
-  rf_status wst = status_of(v, o.err_kind, bad.kind == 2 ? "deintegrate" : "integrate");
-  if (o.err_kind == kErrInconsistent && bad.kind == 2 && bad.entry > 0) {
+  r.failed_window = bad.window;
+  long long wbase = 0;
+  for (int w = 0; w < bad.window; ++w) {
+    wbase += sizes[w];
+    r.n_corrected += sizes[w];
+  }
+  rf_status wst = status_of(v, out.err_kind, bad.kind == 2 ? "deintegrate" : "integrate");
+  if (out.err_kind == kErrInconsistent && bad.kind == 2 && bad.entry > 0) {
     // reintegration.py:170-174: re-integrate what was already removed
     const std::string msg = v->err;
     Batch rb;
     st = batch_begin(v, rb, 2 * bad.entry);
     if (st != RF_OK) return st;
     for (int i = 0; i < bad.entry; ++i) {
-      op_stream(rb, old_poses[i].t);
-      op_fuse(rb, &kfs[i], &old_poses[i], 0, i);
+      op_stream(rb, old_poses[wbase + i].t);
+      op_fuse(rb, &kfs[wbase + i], &old_poses[wbase + i], 0, i);
     }
     BatchOutcome ro;
     st = batch_end(rb, ro);
@@ -679,6 +716,13 @@ rf_status rf_correct(rf_volume* v, int32_t m, const rf_kf_view* kfs, const rf_po
   r.status = wst;
   if (result) *result = r;
   return wst;
+}
+
+rf_status rf_correct(rf_volume* v, int32_t m, const rf_kf_view* kfs, const rf_pose* old_poses,
+                     const rf_pose* new_poses, const double* next_center,
+                     rf_window_result* result) {
+  if (m < 0) return RF_INVALID_ARG;
+  return rf_correct_windows(v, 1, &m, kfs, old_poses, new_poses, next_center, result);
 }
 
 rf_status rf_garbage_collect(rf_volume* v, int64_t* freed) {

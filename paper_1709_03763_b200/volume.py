@@ -495,19 +495,25 @@ def total_weight(store):
     return float(out.value)
 
 
-def correct_entries(store, entries, cfg, next_center=None):
-    """Batched reintegration._correct_entries (reintegration.py:156-181) plus
-    the optional stream(next_center) of correct_window: one native call, one
-    host synchronisation.  Advances entry.integrated_pose on success."""
+def correct_windows(store, windows, cfg, next_center=None):
+    """Back-to-back reintegration._correct_entries calls (reintegration.py:
+    156-181), one per window of ledger entries, followed by the optional
+    stream(next_center) of correct_window / correct_topk -- one native call
+    (rf_correct_windows) and ONE host synchronisation for all of them.
+    Advances entry.integrated_pose exactly where the sequential reference
+    calls would have; raises the reference's exceptions."""
+    windows = [list(w) for w in windows]
+    entries = [e for w in windows for e in w]
     if not entries:
         if next_center is not None:
             stream(store, next_center, cfg)
         return 0
     store._bind(cfg)
-    m = len(entries)
-    views = (L.RfKfView * m)()
-    olds = (L.RfPose * m)()
-    news = (L.RfPose * m)()
+    n = len(entries)
+    views = (L.RfKfView * n)()
+    olds = (L.RfPose * n)()
+    news = (L.RfPose * n)()
+    sizes = (ctypes.c_int32 * len(windows))(*[len(w) for w in windows])
     keep = []
     for i, e in enumerate(entries):
         v, k = kf_view(e.kf, store.device)
@@ -521,19 +527,27 @@ def correct_entries(store, entries, cfg, next_center=None):
         nc = nca.ctypes.data_as(L.c_double_p)
     res = L.RfWindowResult()
     try:
-        store._call("rf_correct", m, views, olds, news, nc, ctypes.byref(res))
-    except StreamingContractError:
-        # reference order: entries integrated before the failing one were
-        # already advanced (reintegration.py:176-179)
-        if res.failed_phase == 1:
-            for e in entries[: res.failed_entry]:
+        store._call("rf_correct_windows", len(windows), sizes, views, olds, news, nc,
+                    ctypes.byref(res))
+    except (StreamingContractError, VolumeInconsistencyError, CapacityError):
+        for w in windows[: max(res.failed_window, 0)]:
+            for e in w:
+                e.integrated_pose = e.target_pose.copy()
+        if res.failed_window >= 0 and res.failed_phase == 1:
+            # reintegration.py:176-179 advanced the entries integrated before
+            for e in windows[res.failed_window][: res.failed_entry]:
                 e.integrated_pose = e.target_pose.copy()
         raise
     finally:
         del keep
     for e in entries:
         e.integrated_pose = e.target_pose.copy()
-    return m
+    return n
+
+
+def correct_entries(store, entries, cfg, next_center=None):
+    """One reintegration._correct_entries window (+ optional next_center)."""
+    return correct_windows(store, [entries], cfg, next_center)
 
 
 # ---------------------------------------------------------------------------
