@@ -204,6 +204,13 @@ rf_status rf_fuse_block(double *d, double *w, double *c,
 rf_status rf_profile_begin(rf_volume *vol);
 rf_status rf_profile_end(rf_volume *vol, rf_profile *out);
 
+/* ---- self-tests --------------------------------------------------------- */
+/* Compare the kernels' shared-denominator division (Markstein correction)
+ * with the IEEE double division on n random operand pairs whose exponents
+ * span [-exp_span, exp_span]; *mismatches = differing bit patterns. */
+rf_status rf_selftest_division(uint64_t n, uint64_t seed, int32_t exp_span,
+                               uint64_t *mismatches);
+
 /* ---- synthetic data (measurement infrastructure, synth.py:46-283) ------ */
 typedef struct rf_synth_prim {
     int32_t kind;        /* 0 Sphere (size[0] = radius), 1 BoxSolid, 2 RoomShell */

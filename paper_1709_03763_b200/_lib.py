@@ -174,6 +174,8 @@ SIGNATURES = {
                       + [c_double_p] + [ctypes.c_double] * 7 + [ctypes.c_int32] * 2
                       + [c_double_p] * 3 + [ctypes.c_double] * 2
                       + [ctypes.c_int32, c_int32_p]),
+    "rf_selftest_division": (_S, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
+                                  ctypes.POINTER(ctypes.c_uint64)]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
     "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4

@@ -147,6 +147,7 @@ struct OpInfo {
 struct Batch {
   rf_volume* v;
   int n_ops = 0;
+  int max_ops = 0;  // op records reset by batch_begin; exceeding it is a bug
   bool has_center;
   double center[3];
   std::vector<PendingStream> streams;
@@ -170,6 +171,7 @@ rf_status batch_begin(rf_volume* v, Batch& b, int max_ops) {
   rf_status st = ensure_ops(v, max_ops);
   if (st != RF_OK) return st;
   b.v = v;
+  b.max_ops = std::max(max_ops, 1);
   b.has_center = v->has_center;
   std::memcpy(b.center, v->center, sizeof(b.center));
   const int n = std::max(max_ops, 1);
@@ -178,9 +180,17 @@ rf_status batch_begin(rf_volume* v, Batch& b, int max_ops) {
   return RF_OK;
 }
 
+int next_op(Batch& b) {
+  if (b.n_ops >= b.max_ops) {
+    std::fprintf(stderr, "refusion_b200: op record overflow (%d >= %d)\n", b.n_ops, b.max_ops);
+    std::abort();
+  }
+  return b.n_ops++;
+}
+
 void op_stream(Batch& b, const double c[3]) {
   rf_volume* v = b.v;
-  const int op = b.n_ops++;
+  const int op = next_op(b);
   b.infos.push_back({0, -1});
   b.fparams.emplace_back();
   StreamParams p{};
@@ -256,7 +266,7 @@ int footprint_grid(rf_volume* v, const rf_kf_view* kf) {
 // mode: 0 integrate, 1 deintegrate, 2 allocate only
 void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
-  const int op = b.n_ops++;
+  const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
   {
@@ -290,7 +300,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
 
 void op_gc(Batch& b) {
   rf_volume* v = b.v;
-  const int op = b.n_ops++;
+  const int op = next_op(b);
   b.infos.push_back({3, -1});
   b.fparams.emplace_back();
   b.gc_op = op;
@@ -637,7 +647,8 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
   r.failed_phase = -1;
   r.failed_window = -1;
   Batch b;
-  rf_status st = batch_begin(v, b, static_cast<int>(4 * total + 2 * n_windows + 2));
+  // per window: stream(old0) + m x (stream, deint) + stream(new0) + m x (stream, int) + gc
+  rf_status st = batch_begin(v, b, static_cast<int>(4 * total + 3 * n_windows + 1));
   if (st != RF_OK) return st;
   // each window is reintegration._correct_entries (reintegration.py:156-181)
   long long base = 0;
@@ -956,6 +967,21 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
   cudaFree(d_kc);
   cudaFree(d_cnt);
   return st;
+}
+
+rf_status rf_selftest_division(uint64_t n, uint64_t seed, int32_t exp_span, uint64_t* mismatches) {
+  if (!mismatches || exp_span < 0 || exp_span > 1000) return RF_INVALID_ARG;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return RF_CUDA;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  k_selftest_division<<<148 * 8, 256>>>(n, seed, exp_span, d);
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  const cudaError_t e = cudaGetLastError();
+  cudaFree(d);
+  if (e != cudaSuccess) return RF_CUDA;
+  *mismatches = h;
+  return RF_OK;
 }
 
 rf_status rf_profile_begin(rf_volume* v) {

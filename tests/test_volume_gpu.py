@@ -268,3 +268,17 @@ def test_save_load_roundtrip(V, tmp_path):
     assert V.compare_volumes(store, loaded) == (0.0, 0.0, 0.0)
     V.stream(loaded, np.zeros(3), cfg)  # binds and uploads
     assert V.compare_volumes(store, loaded) == (0.0, 0.0, 0.0)
+
+
+@pytest.mark.parametrize("exp_span", [8, 60, 600])
+def test_shared_denominator_division_is_ieee(exp_span):
+    """The kernels divide by Markstein correction with a shared reciprocal;
+    it must reproduce IEEE division bit for bit (reference: plain C '/')."""
+    import ctypes
+
+    from paper_1709_03763_b200 import _lib as L
+
+    bad = ctypes.c_uint64()
+    assert L.lib().rf_selftest_division(1 << 27, 1234 + exp_span, exp_span,
+                                        ctypes.byref(bad)) == 0
+    assert bad.value == 0
