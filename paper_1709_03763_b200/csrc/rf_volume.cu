@@ -241,6 +241,12 @@ FootprintParams footprint_params(rf_volume* v, const Batch& b, const rf_kf_view*
   return p;
 }
 
+void set_dim_bits(FuseParams& p) {
+  const double w = static_cast<double>(p.kf.width), h = static_cast<double>(p.kf.height);
+  std::memcpy(&p.w_bits, &w, sizeof(w));
+  std::memcpy(&p.h_bits, &h, sizeof(h));
+}
+
 FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, int op) {
   FuseParams p{};
   p.kf = to_view(kf);
@@ -252,6 +258,7 @@ FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
   p.span = kBlockSide * v->cfg.voxel_size;
   p.mu = v->cfg.mu;
   p.eps_w = 1e-9;  // EPS_W, volume.py:26
+  set_dim_bits(p);
   p.op_index = op;
   p.op = v->d_ops + op;
   p.ws = v->d_ws;
@@ -933,6 +940,7 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
     p.voxel_size = voxel_size;
     p.mu = mu;
     p.eps_w = eps_w;
+    set_dim_bits(p);
     int cnt = 0;
     if (remove) {
       k_fuse_single<kCheckRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
