@@ -200,6 +200,12 @@ rf_status rf_fuse_block(double *d, double *w, double *c,
                         const double *kf_color, double mu, double eps_w,
                         int32_t remove, int32_t *count_out);
 
+/* Device memory the footprint memo may use (default 2 GiB; 0 disables it).
+ * The memo keeps, per (keyframe planes, pose), the block keys its footprint
+ * produced, so the matching de-integration skips the ray sampling; a 64-bit
+ * content hash of the depth/weight planes guards against in-place edits. */
+rf_status rf_set_memo_budget(rf_volume *vol, int64_t bytes);
+
 /* ---- measurement -------------------------------------------------------- */
 rf_status rf_profile_begin(rf_volume *vol);
 rf_status rf_profile_end(rf_volume *vol, rf_profile *out);

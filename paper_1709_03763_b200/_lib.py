@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librefusion_b200.so")
+LIB_PATH = os.environ.get("RF_LIB_PATH") or os.path.join(_HERE, "librefusion_b200.so")
 
 RF_OK = 0
 RF_STREAMING_CONTRACT = 1
@@ -176,6 +176,7 @@ SIGNATURES = {
                       + [ctypes.c_int32, c_int32_p]),
     "rf_selftest_division": (_S, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
                                   ctypes.POINTER(ctypes.c_uint64)]),
+    "rf_set_memo_budget": (_S, [_vp, ctypes.c_int64]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
     "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4

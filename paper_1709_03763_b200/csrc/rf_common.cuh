@@ -73,6 +73,9 @@ struct OpCounters {
   unsigned long long streamed_in;     // stream ops
   unsigned long long streamed_out;
   unsigned long long n_pending;       // distinct missing keys found by k_footprint
+  unsigned long long n_spill;         // tile keys that overflowed shared memory
+  unsigned long long kf_hash;         // content hash of the op's keyframe (memo guard)
+  int use_full;                       // 1: the full footprint kernel must run
   long long viol_key;                 // min footprint key outside the sphere (contract)
   long long fail_key;                 // min key whose removal check failed
   int executed;                       // 1 once the op's first kernel ran
@@ -112,6 +115,8 @@ struct Table {
   long long* pend_keys;  // distinct pending keys of the current op
   int* pend_idx;         // their pend_tab index
   int pend_mask;         // pend_tab size - 1 (power of two)
+  long long* spill_keys; // tile keys that did not fit in shared memory
+  int spill_cap;
   AllocState* alloc;
   long long buckets;
   int capacity;

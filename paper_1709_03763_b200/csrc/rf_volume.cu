@@ -13,6 +13,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <list>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -28,10 +30,38 @@ namespace {
 constexpr int kMaxWindowOps = 4096;
 // distinct new blocks one (de)integration may create (load factor stays low)
 constexpr int kPendingSlots = 1 << 20;
+// tile keys beyond a tile's shared-memory list (only pathological tiles)
+constexpr int kSpillSlots = 1 << 20;
 
 struct EventPair {
   cudaEvent_t a, b;
   int kind;  // 0 fuse, 1 check, 2 footprint
+};
+
+// Host index of the footprint memo: (keyframe planes, intrinsics, pose) ->
+// a device FpEntry holding that footprint's keys (see rf_kernels.cuh).
+struct MemoKey {
+  const void* depth;
+  const void* weight;
+  int width, height;
+  double intr[4];
+  double R[9], t[3];
+  bool operator==(const MemoKey& o) const { return std::memcmp(this, &o, sizeof(MemoKey)) == 0; }
+};
+
+struct MemoKeyHash {
+  size_t operator()(const MemoKey& k) const {
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(&k);
+    unsigned long long h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(MemoKey); ++i) h = (h ^ p[i]) * 1099511628211ull;
+    return static_cast<size_t>(h);
+  }
+};
+
+struct MemoSlot {
+  FpEntry* dev = nullptr;  // descriptor + keys in one allocation
+  size_t bytes = 0;
+  std::list<MemoKey>::iterator lru;
 };
 
 }  // namespace
@@ -60,6 +90,11 @@ struct rf_volume {
   int fuse_grid = 148 * 2;
   int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
   int fp_grid_cap = 148 * 8;
+  // footprint memo
+  std::unordered_map<MemoKey, MemoSlot, MemoKeyHash> memo;
+  std::list<MemoKey> memo_lru;
+  size_t memo_bytes = 0;
+  size_t memo_budget = size_t(2) << 30;
   // profiling
   bool profiling = false;
   std::vector<EventPair> events;
@@ -266,8 +301,74 @@ FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
 }
 
 int footprint_grid(rf_volume* v, const rf_kf_view* kf) {
+  const long long tiles = static_cast<long long>((kf->width + kTile - 1) / kTile) *
+                          ((kf->height + kTile - 1) / kTile);
+  return static_cast<int>(std::max(1LL, std::min<long long>(tiles, v->fp_grid_cap)));
+}
+
+MemoKey memo_key(const rf_kf_view* kf, const rf_pose* pose) {
+  MemoKey k;
+  std::memset(&k, 0, sizeof(k));
+  k.depth = kf->depth;
+  k.weight = kf->weight;
+  k.width = kf->width;
+  k.height = kf->height;
+  k.intr[0] = kf->fx;
+  k.intr[1] = kf->fy;
+  k.intr[2] = kf->cx;
+  k.intr[3] = kf->cy;
+  std::memcpy(k.R, pose->R, sizeof(k.R));
+  std::memcpy(k.t, pose->t, sizeof(k.t));
+  return k;
+}
+
+void memo_evict_lru(rf_volume* v) {
+  const MemoKey& old = v->memo_lru.back();
+  auto it = v->memo.find(old);
+  if (it != v->memo.end()) {
+    cudaFreeAsync(it->second.dev, v->stream);
+    v->memo_bytes -= it->second.bytes;
+    v->memo.erase(it);
+  }
+  v->memo_lru.pop_back();
+}
+
+// Returns the memo entry for (kf, pose) and whether it pre-existed.
+FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bool& existed) {
+  existed = false;
+  if (v->memo_budget == 0) return nullptr;
+  const MemoKey key = memo_key(kf, pose);
+  auto it = v->memo.find(key);
+  if (it != v->memo.end()) {
+    v->memo_lru.splice(v->memo_lru.begin(), v->memo_lru, it->second.lru);
+    existed = true;
+    return it->second.dev;
+  }
   const long long npix = static_cast<long long>(kf->width) * kf->height;
-  return static_cast<int>(std::max(1LL, std::min<long long>((npix + 255) / 256, v->fp_grid_cap)));
+  const int cap = static_cast<int>(std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
+  const size_t bytes = sizeof(FpEntry) + 16 + sizeof(long long) * static_cast<size_t>(cap);
+  if (bytes > v->memo_budget) return nullptr;
+  while (v->memo_bytes + bytes > v->memo_budget && !v->memo_lru.empty()) memo_evict_lru(v);
+  void* mem = nullptr;
+  if (cudaMallocAsync(&mem, bytes, v->stream) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  FpEntry h{};
+  h.keys = reinterpret_cast<long long*>(static_cast<char*>(mem) + ((sizeof(FpEntry) + 15) & ~size_t(15)));
+  h.cap = cap;
+  h.valid = 0;
+  FpEntry* dev = static_cast<FpEntry*>(mem);
+  // the descriptor is pageable host data: copy synchronously w.r.t. the host
+  cudaMemcpyAsync(dev, &h, sizeof(FpEntry), cudaMemcpyHostToDevice, v->stream);
+  v->memo_lru.push_front(key);
+  MemoSlot slot;
+  slot.dev = dev;
+  slot.bytes = bytes;
+  slot.lru = v->memo_lru.begin();
+  v->memo.emplace(key, slot);
+  v->memo_bytes += bytes;
+  return dev;
 }
 
 // mode: 0 integrate, 1 deintegrate, 2 allocate only
@@ -276,16 +377,37 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
+  bool existed = false;
+  FpEntry* memo = memo_lookup(v, kf, pose, existed);
+  int launches = 0;
   {
     ProfScope ps(v, 2);
+    if (memo) {
+      const long long npix = static_cast<long long>(kf->width) * kf->height;
+      k_kf_hash<<<v->n_sms * 2, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
+                                                      &v->d_ops[op].kf_hash);
+      fp.kf_hash = &v->d_ops[op].kf_hash;
+      fp.use_full = &v->d_ops[op].use_full;
+      fp.memo = memo;
+      launches += 1;
+      if (existed) {
+        k_footprint_cached<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
+        launches += 1;
+      }
+    }
     k_footprint<false><<<footprint_grid(v, kf), 256, 0, v->stream>>>(v->T, fp);
+    k_resolve_spill<<<v->n_sms, 256, 0, v->stream>>>(v->T, fp);
     k_commit<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
+    launches += 3;
   }
   FuseParams p = fuse_params(v, kf, pose, op);
+  p.capture = memo;
   b.fparams.push_back(p);
+  b.fparams.back().capture = nullptr;  // the fix-up relaunch must not re-capture
   if (mode == 2) {
     p.alloc_only = 1;
     k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
   if (mode == 0) {
@@ -296,12 +418,13 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
       ProfScope ps(v, 1);
       k_fuse<kCheckRemove><<<v->fuse_grids[kCheckRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
     }
+    p.capture = nullptr;
     ProfScope ps(v, 0);
     k_fuse<kApplyRemove><<<v->fuse_grids[kApplyRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
   }
   if (v->profiling) {
     v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
-    v->prof_launches += mode == 1 ? 4 : 3;
+    v->prof_launches += launches + (mode == 1 ? 2 : 1);
   }
 }
 
@@ -450,6 +573,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   T.buckets = cfg->hash_buckets;
   T.capacity = static_cast<int>(cap);
   T.pend_mask = kPendingSlots - 1;
+  T.spill_cap = kSpillSlots;
   auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes) == cudaSuccess; };
   bool ok = alloc(reinterpret_cast<void**>(&T.heads), sizeof(int) * cfg->hash_buckets) &&
             alloc(reinterpret_cast<void**>(&T.keys), sizeof(long long) * cap) &&
@@ -463,6 +587,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
             alloc(reinterpret_cast<void**>(&T.pend_tab), sizeof(long long) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.pend_keys), sizeof(long long) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.pend_idx), sizeof(int) * kPendingSlots) &&
+            alloc(reinterpret_cast<void**>(&T.spill_keys), sizeof(long long) * kSpillSlots) &&
             alloc(reinterpret_cast<void**>(&T.alloc), sizeof(AllocState)) &&
             alloc(reinterpret_cast<void**>(&T.pool), sizeof(double) * kBlockDoubles * cap) &&
             alloc(reinterpret_cast<void**>(&v->d_ws), sizeof(WinState)) &&
@@ -497,7 +622,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
   cudaDeviceSynchronize();
   Table& T = v->T;
   void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched,
-                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums};
+                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {v->h_ws, v->h_u64, v->h_f64, v->h_alloc, v->h_ops};
@@ -508,6 +633,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
     cudaEventDestroy(e.b);
   }
   for (auto e : v->event_pool) cudaEventDestroy(e);
+  for (auto& kv : v->memo) cudaFree(kv.second.dev);
   delete v;
   return RF_OK;
 }
@@ -989,6 +1115,14 @@ rf_status rf_selftest_division(uint64_t n, uint64_t seed, int32_t exp_span, uint
   cudaFree(d);
   if (e != cudaSuccess) return RF_CUDA;
   *mismatches = h;
+  return RF_OK;
+}
+
+rf_status rf_set_memo_budget(rf_volume* v, int64_t bytes) {
+  if (!v || bytes < 0) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  v->memo_budget = static_cast<size_t>(bytes);
+  while (v->memo_bytes > v->memo_budget && !v->memo_lru.empty()) memo_evict_lru(v);
   return RF_OK;
 }
 
