@@ -210,6 +210,67 @@ rf_status rf_set_memo_budget(rf_volume *vol, int64_t bytes);
 rf_status rf_profile_begin(rf_volume *vol);
 rf_status rf_profile_end(rf_volume *vol, rf_profile *out);
 
+/* ---- keyframe fusion (keyframe_fusion.py:142-460) ---------------------- */
+/* Multiply-add order of the host BLAS behind geometry.transform
+ * (p @ R.T + t, src/refusion/geometry.py:101-104): the reference's fused
+ * depth depends on it, so it is calibrated on the host and passed in. */
+typedef enum rf_blas_order {
+    RF_BLAS_PLAIN = 0,    /* (p0 r0 + p1 r1) + p2 r2, no FMA */
+    RF_BLAS_FMA_210 = 1,  /* fma(p2, r2, fma(p1, r1, p0 r0)) (OpenBLAS SkylakeX dgemm) */
+    RF_BLAS_FMA_012 = 2,  /* fma(p0, r0, fma(p1, r1, p2 r2)) */
+    RF_BLAS_FMA_201 = 3   /* fma(p2, r2, fma(p0, r0, p1 r1)) */
+} rf_blas_order;
+
+/* depth_sample_weight / discontinuity_mask (keyframe_fusion.py:191-231,
+ * :245-246).  flags = RF_DW_MASK: w_map[h][w] = cos(theta)/Z^2 zeroed at
+ * discontinuities (fuse_depth's weight map); 0: the unmasked weight;
+ * RF_DW_MASK_ONLY: the mask itself as 1.0 / 0.0. */
+enum { RF_DW_MASK = 1, RF_DW_MASK_ONLY = 2 };
+rf_status rf_depth_weight(const double *depth, int32_t width, int32_t height,
+                          double fx, double fy, double cx, double cy,
+                          double delta_disc, int32_t flags, double *w_map, void *stream);
+/* fuse_depth's warp + np.add.at scatter + Eq. 1 merge (keyframe_fusion.py:
+ * 247-276): rel = compose(inverse(kf.pose), frame.pose).  Deterministic:
+ * contributions to a keyframe pixel are summed in source-pixel order. */
+rf_status rf_fuse_depth(double *kf_depth, double *kf_weight, const double *frame_depth,
+                        const double *w_map, int32_t width, int32_t height,
+                        double fx, double fy, double cx, double cy,
+                        const rf_pose *rel, int32_t blas_order, void *stream);
+/* unsharp_mask (keyframe_fusion.py:335-346) of an [h][w][channels] image:
+ * scipy gaussian_filter (mode 'nearest', gauss_weights[2*radius+1] =
+ * _gaussian_kernel1d) per channel, then clip(img + gain*(img - low), 0, 255). */
+rf_status rf_unsharp_mask(const double *img, int32_t width, int32_t height, int32_t channels,
+                          const double *gauss_weights, int32_t radius, double gain,
+                          double *out, void *stream);
+/* grayscale (:303-307) of [h][w][3] */
+rf_status rf_grayscale(const double *color, int32_t width, int32_t height, double *gray,
+                       void *stream);
+/* blurriness (:310-332) of a gray [h][w] image; result is a device scalar */
+rf_status rf_blurriness(const double *gray, int32_t width, int32_t height,
+                        double *blur_weight, void *stream);
+/* fuse_depth's colour prep (:278-281): unsharp mask + blurriness of grayscale */
+rf_status rf_color_prep(const double *color, int32_t width, int32_t height,
+                        const double *gauss_weights, int32_t radius, double gain,
+                        double *member_color, double *blur_weight, void *stream);
+
+/* One retained member observation (_MemberObservation, keyframe_fusion.py:87-96). */
+typedef struct rf_member_view {
+    const double *depth;        /* [h][w] device */
+    const double *w_map;        /* [h][w] device */
+    const double *color;        /* deblurred [h][w][3] device */
+    const double *blur_weight;  /* device scalar */
+    rf_pose rel;                /* compose(inverse(member.pose), kf.pose) */
+} rf_member_view;
+
+/* fuse_color (keyframe_fusion.py:377-460): per-channel blur-weighted
+ * median over <= 64 members; color_valid[h][w] is 0/1. */
+rf_status rf_fuse_color(const double *kf_depth, const double *kf_weight,
+                        int32_t width, int32_t height, double fx, double fy,
+                        double cx, double cy, int32_t n_members,
+                        const rf_member_view *members, double delta_occl,
+                        int32_t blas_order, double *kf_color, uint8_t *color_valid,
+                        void *stream);
+
 /* ---- self-tests --------------------------------------------------------- */
 /* Compare the kernels' shared-denominator division (Markstein correction)
  * with the IEEE double division on n random operand pairs whose exponents

@@ -114,6 +114,16 @@ class RfProfile(ctypes.Structure):
     ]
 
 
+class RfMemberView(ctypes.Structure):
+    _fields_ = [
+        ("depth", ctypes.c_void_p),
+        ("w_map", ctypes.c_void_p),
+        ("color", ctypes.c_void_p),
+        ("blur_weight", ctypes.c_void_p),
+        ("rel", RfPose),
+    ]
+
+
 class RfSynthPrim(ctypes.Structure):
     _fields_ = [
         ("kind", ctypes.c_int32),
@@ -174,6 +184,19 @@ SIGNATURES = {
                       + [c_double_p] + [ctypes.c_double] * 7 + [ctypes.c_int32] * 2
                       + [c_double_p] * 3 + [ctypes.c_double] * 2
                       + [ctypes.c_int32, c_int32_p]),
+    "rf_depth_weight": (_S, [_vp, ctypes.c_int32, ctypes.c_int32] + [ctypes.c_double] * 5
+                        + [ctypes.c_int32, _vp, _vp]),
+    "rf_fuse_depth": (_S, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32]
+                      + [ctypes.c_double] * 4 + [ctypes.POINTER(RfPose), ctypes.c_int32, _vp]),
+    "rf_unsharp_mask": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_double_p,
+                             ctypes.c_int32, ctypes.c_double, _vp, _vp]),
+    "rf_grayscale": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
+    "rf_blurriness": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
+    "rf_color_prep": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, c_double_p, ctypes.c_int32,
+                           ctypes.c_double, _vp, _vp, _vp]),
+    "rf_fuse_color": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32] + [ctypes.c_double] * 4
+                      + [ctypes.c_int32, ctypes.POINTER(RfMemberView), ctypes.c_double,
+                         ctypes.c_int32, _vp, _vp, _vp]),
     "rf_selftest_division": (_S, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
                                   ctypes.POINTER(ctypes.c_uint64)]),
     "rf_set_memo_budget": (_S, [_vp, ctypes.c_int64]),

@@ -1,0 +1,693 @@
+// rf_fusion.cu -- keyframe fusion on the device.
+//
+// Reference: /root/reference/pkg/src/refusion/keyframe_fusion.py
+//   :142-231  normal_map / depth_sample_weight / discontinuity_mask  -> k_depth_weight
+//   :238-276  fuse_depth: warp into the keyframe, np.add.at scatter, Eq. 1
+//             -> k_warp, k_count, scan, k_scatter, k_merge (ordered segmented sums)
+//   :278-346  grayscale / unsharp_mask / blurriness                  -> k_gauss_*, k_blur_*
+//   :349-460  fuse_color: blur-weighted per-channel weighted median  -> k_fuse_color
+//
+// Arithmetic follows numpy / scipy operation by operation (compiled with
+// -fmad=false): elementwise ufuncs are single IEEE ops, np.add.at applies
+// in source order, scipy's correlate1d uses its symmetric-kernel loop,
+// uniform_filter1d a running sum divided per output, and ndarray.sum()
+// numpy's pairwise summation.  The one host-dependent step is
+// geometry.transform (p @ R.T + t through BLAS): its multiply-add order is
+// a parameter (rf_blas_order), calibrated on the host at start-up
+// (keyframe_fusion.detect_blas_order).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "refusion_b200.h"
+
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+struct Intr {
+  int w, h;
+  double fx, fy, cx, cy;
+};
+
+// p @ R.T + t for one point, in the host BLAS's order (rf_blas_order)
+__device__ __forceinline__ double blas_row(const double* r, double p0, double p1, double p2,
+                                           int order) {
+  switch (order) {
+    case RF_BLAS_FMA_210: return fma(p2, r[2], fma(p1, r[1], p0 * r[0]));
+    case RF_BLAS_FMA_012: return fma(p0, r[0], fma(p1, r[1], p2 * r[2]));
+    case RF_BLAS_FMA_201: return fma(p2, r[2], fma(p0, r[0], p1 * r[1]));
+    default: return (p0 * r[0] + p1 * r[1]) + p2 * r[2];
+  }
+}
+
+__device__ __forceinline__ void transform(const rf_pose& T, double p0, double p1, double p2,
+                                          int order, double& q0, double& q1, double& q2) {
+  q0 = blas_row(T.R + 0, p0, p1, p2, order) + T.t[0];
+  q1 = blas_row(T.R + 3, p0, p1, p2, order) + T.t[1];
+  q2 = blas_row(T.R + 6, p0, p1, p2, order) + T.t[2];
+}
+
+// ---------------------------------------------------------------------------
+// depth sample weight w_z = cos(theta) / Z^2 with the discontinuity mask
+
+// flags: RF_DW_MASK applies the discontinuity mask to w (fuse_depth's
+// w_map); RF_DW_MASK_ONLY writes the mask itself as 1.0 / 0.0.
+__global__ void k_depth_weight(const double* __restrict__ depth, Intr in, double delta_disc,
+                               int flags, double* __restrict__ w_out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= in.w || v >= in.h) return;
+  const int W = in.w, H = in.h;
+  auto D = [&](int vv, int uu) { return __ldg(&depth[static_cast<size_t>(vv) * W + uu]); };
+  auto dx = [&](int uu) { return (static_cast<double>(uu) - in.cx) / in.fx; };  // ray_grid
+  auto dy = [&](int vv) { return (static_cast<double>(vv) - in.cy) / in.fy; };
+  const double d = D(v, u);
+  // normal_map (:142-188): central differences of unprojected neighbours
+  double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+  if (u >= 1 && u <= W - 2 && v >= 1 && v <= H - 2) {
+    const double dr = D(v, u + 1), dl = D(v, u - 1), dd = D(v + 1, u), du = D(v - 1, u);
+    const double xr = dx(u + 1), xl = dx(u - 1), xc = dx(u);
+    const double yc = dy(v), yd = dy(v + 1), yu = dy(v - 1);
+    const double a0 = xr * dr - xl * dl, a1 = yc * dr - yc * dl, a2 = dr - dl;
+    const double b0 = xc * dd - xc * du, b1 = yd * dd - yu * du, b2 = dd - du;
+    const double c0 = a1 * b2 - a2 * b1;  // np.cross
+    const double c1 = a2 * b0 - a0 * b2;
+    const double c2 = a0 * b1 - a1 * b0;
+    const double nrm = sqrt(c0 * c0 + c1 * c1 + c2 * c2);
+    const bool ok = d > 0 && dr > 0 && dl > 0 && dd > 0 && du > 0 && nrm > 0;
+    if (ok) {
+      n0 = c0 / nrm;
+      n1 = c1 / nrm;
+      n2 = c2 / nrm;
+    }
+  }
+  // depth_sample_weight (:191-208)
+  const double rx = dx(u), ry = dy(v);
+  const double ray_norm = sqrt(rx * rx + ry * ry + 1.0);
+  const double cos_t = (n0 * rx + n1 * ry + n2) / ray_norm;
+  double w = 0.0;
+  if (d > 0 && isfinite(d) && cos_t > 0) w = cos_t / (d * d);
+  // discontinuity_mask (:211-231): invalid, or next to invalid / a jump
+  bool masked = !(d > 0);
+  if (!masked) {
+    for (int sv = -1; sv <= 1 && !masked; ++sv)
+      for (int su = -1; su <= 1; ++su) {
+        if (sv == 0 && su == 0) continue;
+        const int nv = v + sv, nu = u + su;
+        if (nv < 0 || nv >= H || nu < 0 || nu >= W) continue;
+        const double nb = D(nv, nu);
+        if (!(nb > 0) || fabs(d - nb) > delta_disc) {
+          masked = true;
+          break;
+        }
+      }
+  }
+  double out = w;
+  if (flags & RF_DW_MASK_ONLY) out = masked ? 1.0 : 0.0;
+  else if ((flags & RF_DW_MASK) && masked) out = 0.0;
+  w_out[static_cast<size_t>(v) * W + u] = out;
+}
+
+// ---------------------------------------------------------------------------
+// fuse_depth: warp -> ordered scatter -> Eq. 1
+
+__global__ void k_warp(const double* __restrict__ depth, const double* __restrict__ w_map, Intr in,
+                       rf_pose rel, int order, int* __restrict__ target,
+                       double* __restrict__ val_wz, double* __restrict__ val_w,
+                       int* __restrict__ counts) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = in.w * in.h;
+  if (i >= n) return;
+  int t = -1;
+  const double ws = __ldg(&w_map[i]);
+  if (ws > 0.0) {
+    const int u = i % in.w, v = i / in.w;
+    const double z = __ldg(&depth[i]);
+    const double p0 = ((static_cast<double>(u) - in.cx) / in.fx) * z;
+    const double p1 = ((static_cast<double>(v) - in.cy) / in.fy) * z;
+    double q0, q1, q2;
+    transform(rel, p0, p1, z, order, q0, q1, q2);
+    if (q2 > 0) {
+      const double uf = floor(in.fx * q0 / q2 + in.cx + 0.5);
+      const double vf = floor(in.fy * q1 / q2 + in.cy + 0.5);
+      if (uf >= 0 && uf < in.w && vf >= 0 && vf < in.h) {
+        t = static_cast<int>(vf) * in.w + static_cast<int>(uf);
+        val_wz[i] = ws * q2;
+        val_w[i] = ws;
+        atomicAdd(&counts[t], 1);
+      }
+    }
+  }
+  target[i] = t;
+}
+
+// exclusive scan of n ints: per-CTA sums, a single-CTA scan of those, apply
+constexpr int kScanBlock = 1024;
+
+__global__ void k_scan_partial(const int* __restrict__ in, int n, int* __restrict__ sums) {
+  __shared__ int s[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  int v = i < n ? in[i] : 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int k = 0; k < kScanBlock / 32; ++k) t += s[k];
+    sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_scan_sums(int* sums, int m) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    int acc = 0;
+    for (int k = 0; k < m; ++k) {
+      const int v = sums[k];
+      sums[k] = acc;
+      acc += v;
+    }
+  }
+}
+
+__global__ void k_scan_apply(const int* __restrict__ in, int n, const int* __restrict__ sums,
+                             int* __restrict__ out) {
+  __shared__ int s[32];
+  const int i = blockIdx.x * kScanBlock + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int v = i < n ? in[i] : 0;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(kFull, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = s[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(kFull, w, o);
+      if (lane >= o) w += y;
+    }
+    s[lane] = w;
+  }
+  __syncthreads();
+  const int before = (warp > 0 ? s[warp - 1] : 0) + x - v;
+  if (i < n) out[i] = sums[blockIdx.x] + before;
+}
+
+__global__ void k_scatter(const int* __restrict__ target, int n, const int* __restrict__ offsets,
+                          int* __restrict__ cursor, int* __restrict__ slots) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int t = target[i];
+  if (t < 0) return;
+  slots[offsets[t] + atomicAdd(&cursor[t], 1)] = i;
+}
+
+// np.add.at applies contributions in source order: sort each (short)
+// segment by source index, sum sequentially, then the Eq. 1 merge
+// (:270-276).
+__global__ void k_merge(double* __restrict__ kf_depth, double* __restrict__ kf_weight, int n,
+                        const int* __restrict__ counts, const int* __restrict__ offsets,
+                        int* __restrict__ slots, const double* __restrict__ val_wz,
+                        const double* __restrict__ val_w) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int c = counts[t];
+  if (c == 0) return;
+  int* seg = slots + offsets[t];
+  for (int a = 1; a < c; ++a) {  // insertion sort by source index
+    const int key = seg[a];
+    int b = a - 1;
+    while (b >= 0 && seg[b] > key) {
+      seg[b + 1] = seg[b];
+      --b;
+    }
+    seg[b + 1] = key;
+  }
+  double awz = 0.0, aw = 0.0;
+  for (int a = 0; a < c; ++a) {
+    awz = awz + val_wz[seg[a]];
+    aw = aw + val_w[seg[a]];
+  }
+  if (aw > 0) {
+    const double kd = kf_depth[t], kw = kf_weight[t];
+    kf_depth[t] = (kd * kw + awz) / (kw + aw);
+    kf_weight[t] = kw + aw;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// colour prep: grayscale, unsharp mask (scipy gaussian_filter, mode
+// 'nearest', separable: axis 0 then axis 1), blurriness
+
+// scipy correlate1d, symmetric weights: out = x0*w0 + sum_{j=r..1} (x[-j] + x[+j]) * w[j]
+__device__ __forceinline__ double corr_sym(const double* line, int stride, int len, int i,
+                                           const double* w, int r) {
+  double acc = line[static_cast<size_t>(i) * stride] * w[0];
+  for (int j = r; j >= 1; --j) {
+    const int lo = max(i - j, 0), hi = min(i + j, len - 1);  // mode 'nearest'
+    acc = acc + (line[static_cast<size_t>(lo) * stride] + line[static_cast<size_t>(hi) * stride]) * w[j];
+  }
+  return acc;
+}
+
+struct GaussW {
+  double w[16];  // w[0] centre, w[j] = weight at offset j
+  int r;
+};
+
+// pass along axis 0 (vertical) on channel ch of an interleaved (h, w, c) image
+__global__ void k_gauss_rows(const double* __restrict__ img, int W, int H, int C, GaussW g,
+                             double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= W || v >= H) return;
+  for (int ch = 0; ch < C; ++ch)
+    out[(static_cast<size_t>(v) * W + u) * C + ch] =
+        corr_sym(img + static_cast<size_t>(u) * C + ch, W * C, H, v, g.w, g.r);
+}
+
+// pass along axis 1, then unsharp: clip(img + gain * (img - low), 0, 255)
+__global__ void k_gauss_cols_unsharp(const double* __restrict__ img,
+                                     const double* __restrict__ tmp, int W, int H, int C,
+                                     GaussW g, double gain, double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= W || v >= H) return;
+  for (int ch = 0; ch < C; ++ch) {
+    const size_t at = (static_cast<size_t>(v) * W + u) * C + ch;
+    const double low = corr_sym(tmp + static_cast<size_t>(v) * W * C + ch, C, W, u, g.w, g.r);
+    const double x = img[at];
+    const double s = x + gain * (x - low);
+    out[at] = fmin(fmax(s, 0.0), 255.0);  // np.clip (NaN-free inputs)
+  }
+}
+
+__global__ void k_gray(const double* __restrict__ color, int n, double* __restrict__ gray) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const double* c = color + 3 * static_cast<size_t>(i);
+  gray[i] = 0.299 * c[0] + 0.587 * c[1] + 0.114 * c[2];  // :307
+}
+
+// uniform_filter1d(size 9, mode 'nearest') along one axis: running sum,
+// divided per output; then |diff(f)|, |diff(b)| and v = max(0, d_f - d_b)
+// written flattened row-major for the pairwise sums.  One thread per line.
+__global__ void k_blur_lines(const double* __restrict__ f, int W, int H, int axis, int size,
+                             double* __restrict__ b, double* __restrict__ d_f,
+                             double* __restrict__ vv) {
+  const int line = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lines = axis == 0 ? W : H;
+  if (line >= lines) return;
+  const int len = axis == 0 ? H : W;
+  const size_t stride = axis == 0 ? W : 1;
+  const double* src = f + (axis == 0 ? line : static_cast<size_t>(line) * W);
+  double* dst = b + (axis == 0 ? line : static_cast<size_t>(line) * W);
+  const int s1 = size / 2;
+  auto at = [&](int k) { return src[static_cast<size_t>(min(max(k, 0), len - 1)) * stride]; };
+  double tmp = 0.0;
+  for (int l = 0; l < size; ++l) tmp = tmp + at(l - s1);
+  dst[0] = tmp / size;
+  for (int l = 1; l < len; ++l) {
+    tmp = tmp + (at(l + size - 1 - s1) - at(l - 1 - s1));
+    dst[static_cast<size_t>(l) * stride] = tmp / size;
+  }
+  // diffs along the axis, flattened as numpy lays them out: (H-1, W) or (H, W-1)
+  for (int l = 0; l + 1 < len; ++l) {
+    const double df = fabs(src[static_cast<size_t>(l + 1) * stride] - src[static_cast<size_t>(l) * stride]);
+    const double db = fabs(dst[static_cast<size_t>(l + 1) * stride] - dst[static_cast<size_t>(l) * stride]);
+    const size_t o = axis == 0 ? static_cast<size_t>(l) * W + line : static_cast<size_t>(line) * (W - 1) + l;
+    d_f[o] = df;
+    vv[o] = fmax(0.0, df - db);
+  }
+}
+
+// numpy pairwise summation (pairwise_sum in loops_utils.h): blocks of <=128
+// elements with 8 accumulators, recursive halving at multiples of 8.
+__device__ double pairwise_leaf(const double* a, long long n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (long long i = 0; i < n; ++i) r = r + a[i];
+    return r;
+  }
+  double r[8];
+  for (int k = 0; k < 8; ++k) r[k] = a[k];
+  long long i = 8;
+  for (; i < n - (n % 8); i += 8)
+    for (int k = 0; k < 8; ++k) r[k] = r[k] + a[i + k];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res = res + a[i];
+  return res;
+}
+
+// the recursion tree is fixed by n: leaves are evaluated in parallel, then
+// combined bottom-up in the recursion's pairing order by one thread
+struct PwNode {
+  long long off, n;
+  int left, right;  // children, -1 for a leaf
+  double val;
+};
+
+__global__ void k_pairwise_leaves(const double* a, PwNode* nodes, int n_nodes) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n_nodes || nodes[k].left >= 0) return;
+  nodes[k].val = pairwise_leaf(a + nodes[k].off, nodes[k].n);
+}
+
+__global__ void k_pairwise_combine(PwNode* nodes, int n_nodes, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  // nodes are stored so that children precede parents (post-order)
+  for (int k = 0; k < n_nodes; ++k)
+    if (nodes[k].left >= 0) nodes[k].val = nodes[nodes[k].left].val + nodes[nodes[k].right].val;
+  *out = nodes[n_nodes - 1].val;
+}
+
+// blurriness (:310-332): scores (s_f - v.sum()) / s_f per axis with s_f > 0
+__global__ void k_blur_finish(const double* sums, int n_axes, double* blur_weight) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  bool any = false;
+  double best = 0.0;
+  for (int a = 0; a < n_axes; ++a) {
+    const double s_f = sums[2 * a], s_v = sums[2 * a + 1];
+    if (s_f > 0) {
+      const double sc = (s_f - s_v) / s_f;
+      if (!any || sc > best) best = sc;  // Python max(): first maximum wins
+      any = true;
+    }
+  }
+  if (!any) {
+    *blur_weight = 1.0;
+    return;
+  }
+  *blur_weight = fmin(fmax(1.0 - best, 0.0), 1.0);
+}
+
+// ---------------------------------------------------------------------------
+// fuse_color (:377-460)
+
+constexpr int kMaxMembers = 64;
+
+struct MemberDev {
+  const double* depth;
+  const double* w_map;
+  const double* color;
+  const double* blur;
+  rf_pose rel;
+};
+
+__device__ __forceinline__ void bilinear(const double* img, int W, int H, double u, double v,
+                                         double out[3]) {  // _bilinear (:362-374)
+  long long u0 = static_cast<long long>(floor(u)), v0 = static_cast<long long>(floor(v));
+  u0 = min(max(u0, 0LL), static_cast<long long>(W - 1));
+  v0 = min(max(v0, 0LL), static_cast<long long>(H - 1));
+  const long long u1 = min(u0 + 1, static_cast<long long>(W - 1));
+  const long long v1 = min(v0 + 1, static_cast<long long>(H - 1));
+  const double fu = u - static_cast<double>(u0), fv = v - static_cast<double>(v0);
+  for (int c = 0; c < 3; ++c) {
+    const double a = img[(v0 * W + u0) * 3 + c], b = img[(v0 * W + u1) * 3 + c];
+    const double d = img[(v1 * W + u0) * 3 + c], e = img[(v1 * W + u1) * 3 + c];
+    const double top = a * (1 - fu) + b * fu;
+    const double bot = d * (1 - fu) + e * fu;
+    out[c] = top * (1 - fv) + bot * fv;
+  }
+}
+
+__global__ void k_fuse_color(const double* __restrict__ kd, const double* __restrict__ kw, Intr in,
+                             const MemberDev* __restrict__ mem, int n_mem, double delta_occl,
+                             int order, double* __restrict__ color_out,
+                             unsigned char* __restrict__ valid_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= in.w * in.h) return;
+  double* co = color_out + 3 * static_cast<size_t>(i);
+  co[0] = co[1] = co[2] = 0.0;
+  valid_out[i] = 0;
+  if (!(kw[i] > 0.0)) return;
+  const int u = i % in.w, v = i / in.w;
+  const double z = kd[i];
+  const double p0 = ((static_cast<double>(u) - in.cx) / in.fx) * z;
+  const double p1 = ((static_cast<double>(v) - in.cy) / in.fy) * z;
+  double vals[kMaxMembers][3];
+  double wts[kMaxMembers];
+  for (int m = 0; m < n_mem; ++m) {
+    vals[m][0] = vals[m][1] = vals[m][2] = 0.0;
+    wts[m] = 0.0;
+    const MemberDev& M = mem[m];
+    double q0, q1, q2;
+    transform(M.rel, p0, p1, z, order, q0, q1, q2);
+    if (!(q2 > 0)) continue;
+    const double uu = in.fx * q0 / q2 + in.cx;
+    const double vv = in.fy * q1 / q2 + in.cy;
+    if (!(uu >= 0 && uu <= in.w - 1 && vv >= 0 && vv <= in.h - 1)) continue;
+    const int un = static_cast<int>(floor(uu + 0.5)), vn = static_cast<int>(floor(vv + 0.5));
+    const size_t q = static_cast<size_t>(vn) * in.w + un;
+    const double zn = M.depth[q];
+    const double w_c = *M.blur * M.w_map[q];
+    if (!(zn > 0 && fabs(zn - q2) <= delta_occl && w_c > 0)) continue;
+    bilinear(M.color, in.w, in.h, uu, vv, vals[m]);
+    wts[m] = w_c;
+  }
+  double total = 0.0;
+  for (int m = 0; m < n_mem; ++m) total = total + wts[m];  // sum(axis=0)
+  if (!(total > 0)) return;
+  const double half = total / 2.0;
+  int idx[kMaxMembers];
+  for (int ch = 0; ch < 3; ++ch) {
+    for (int m = 0; m < n_mem; ++m) idx[m] = m;
+    for (int a = 1; a < n_mem; ++a) {  // stable insertion sort by value
+      const int key = idx[a];
+      const double kv = vals[key][ch];
+      int b = a - 1;
+      while (b >= 0 && vals[idx[b]][ch] > kv) {
+        idx[b + 1] = idx[b];
+        --b;
+      }
+      idx[b + 1] = key;
+    }
+    double cum = 0.0;
+    int pick = 0;  // argmax of (cum >= half): first True, else 0
+    for (int a = 0; a < n_mem; ++a) {
+      cum = cum + wts[idx[a]];
+      if (cum >= half) {
+        pick = a;
+        break;
+      }
+    }
+    co[ch] = vals[idx[pick]][ch];
+  }
+  valid_out[i] = 1;
+}
+
+Intr make_intr(int w, int h, double fx, double fy, double cx, double cy) {
+  Intr in;
+  in.w = w;
+  in.h = h;
+  in.fx = fx;
+  in.fy = fy;
+  in.cx = cx;
+  in.cy = cy;
+  return in;
+}
+
+int build_pairwise_tree(long long off, long long n, std::vector<PwNode>& out) {
+  if (n <= 128) {
+    out.push_back({off, n, -1, -1, 0.0});
+    return static_cast<int>(out.size()) - 1;
+  }
+  long long n2 = n / 2;
+  n2 -= n2 % 8;
+  const int l = build_pairwise_tree(off, n2, out);
+  const int r = build_pairwise_tree(off + n2, n - n2, out);
+  out.push_back({off, n, l, r, 0.0});
+  return static_cast<int>(out.size()) - 1;
+}
+
+rf_status pairwise_sum(const double* a, long long n, double* out, cudaStream_t s) {
+  std::vector<PwNode> nodes;
+  build_pairwise_tree(0, n, nodes);
+  PwNode* d = nullptr;
+  if (cudaMallocAsync(&d, sizeof(PwNode) * nodes.size(), s) != cudaSuccess) return RF_CUDA;
+  cudaMemcpyAsync(d, nodes.data(), sizeof(PwNode) * nodes.size(), cudaMemcpyHostToDevice, s);
+  const int nn = static_cast<int>(nodes.size());
+  k_pairwise_leaves<<<(nn + 127) / 128, 128, 0, s>>>(a, d, nn);
+  k_pairwise_combine<<<1, 1, 0, s>>>(d, nn, out);
+  cudaFreeAsync(d, s);
+  return RF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+rf_status rf_depth_weight(const double* depth, int32_t width, int32_t height, double fx, double fy,
+                          double cx, double cy, double delta_disc, int32_t flags, double* w_map,
+                          void* stream) {
+  if (!depth || !w_map || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  dim3 blk(32, 8), grd((width + 31) / 32, (height + 7) / 8);
+  k_depth_weight<<<grd, blk, 0, s>>>(depth, make_intr(width, height, fx, fy, cx, cy), delta_disc,
+                                     flags, w_map);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_fuse_depth(double* kf_depth, double* kf_weight, const double* frame_depth,
+                        const double* w_map, int32_t width, int32_t height, double fx, double fy,
+                        double cx, double cy, const rf_pose* rel, int32_t blas_order,
+                        void* stream) {
+  if (!kf_depth || !kf_weight || !frame_depth || !w_map || !rel || width <= 0 || height <= 0)
+    return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = width * height;
+  const int nb = (n + kScanBlock - 1) / kScanBlock;
+  int *target = nullptr, *counts = nullptr, *offsets = nullptr, *cursor = nullptr,
+      *slots = nullptr, *sums = nullptr;
+  double *vwz = nullptr, *vw = nullptr;
+  bool ok = cudaMallocAsync(&target, sizeof(int) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&counts, sizeof(int) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&offsets, sizeof(int) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&cursor, sizeof(int) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&slots, sizeof(int) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&sums, sizeof(int) * (nb + 1), s) == cudaSuccess &&
+            cudaMallocAsync(&vwz, sizeof(double) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&vw, sizeof(double) * n, s) == cudaSuccess;
+  if (ok) {
+    cudaMemsetAsync(counts, 0, sizeof(int) * n, s);
+    cudaMemsetAsync(cursor, 0, sizeof(int) * n, s);
+    const Intr in = make_intr(width, height, fx, fy, cx, cy);
+    k_warp<<<(n + 255) / 256, 256, 0, s>>>(frame_depth, w_map, in, *rel, blas_order, target, vwz,
+                                            vw, counts);
+    k_scan_partial<<<nb, kScanBlock, 0, s>>>(counts, n, sums);
+    k_scan_sums<<<1, 32, 0, s>>>(sums, nb);
+    k_scan_apply<<<nb, kScanBlock, 0, s>>>(counts, n, sums, offsets);
+    k_scatter<<<(n + 255) / 256, 256, 0, s>>>(target, n, offsets, cursor, slots);
+    k_merge<<<(n + 255) / 256, 256, 0, s>>>(kf_depth, kf_weight, n, counts, offsets, slots, vwz, vw);
+  }
+  void* bufs[] = {target, counts, offsets, cursor, slots, sums, vwz, vw};
+  for (void* b : bufs)
+    if (b) cudaFreeAsync(b, s);
+  if (!ok) return RF_CUDA;
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_unsharp_mask(const double* img, int32_t width, int32_t height, int32_t channels,
+                          const double* gauss_weights, int32_t radius, double gain, double* out,
+                          void* stream) {
+  if (!img || !out || !gauss_weights || width <= 0 || height <= 0 || channels <= 0 ||
+      radius < 0 || radius > 15)
+    return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n = static_cast<long long>(width) * height * channels;
+  if (gain == 0.0) {  // unsharp_mask returns img.copy() (:338-339)
+    cudaMemcpyAsync(out, img, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+  }
+  GaussW g;
+  g.r = radius;
+  for (int j = 0; j <= radius; ++j) g.w[j] = gauss_weights[radius + j];  // symmetric
+  double* tmp = nullptr;
+  if (cudaMallocAsync(&tmp, sizeof(double) * n, s) != cudaSuccess) return RF_CUDA;
+  dim3 blk(32, 8), grd((width + 31) / 32, (height + 7) / 8);
+  k_gauss_rows<<<grd, blk, 0, s>>>(img, width, height, channels, g, tmp);
+  k_gauss_cols_unsharp<<<grd, blk, 0, s>>>(img, tmp, width, height, channels, g, gain, out);
+  cudaFreeAsync(tmp, s);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_grayscale(const double* color, int32_t width, int32_t height, double* gray,
+                       void* stream) {
+  if (!color || !gray || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  const int n = width * height;
+  k_gray<<<(n + 255) / 256, 256, 0, static_cast<cudaStream_t>(stream)>>>(color, n, gray);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_blurriness(const double* gray, int32_t width, int32_t height, double* blur_weight,
+                        void* stream) {
+  if (!gray || !blur_weight || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long n = static_cast<long long>(width) * height;
+  double *b = nullptr, *d_f = nullptr, *vv = nullptr, *sums = nullptr;
+  bool ok = cudaMallocAsync(&b, sizeof(double) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&d_f, sizeof(double) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&vv, sizeof(double) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&sums, sizeof(double) * 4, s) == cudaSuccess;
+  rf_status st = ok ? RF_OK : RF_CUDA;
+  if (ok) {
+    int axes = 0;
+    double* sum_ptr = sums;
+    for (int axis = 0; axis < 2; ++axis) {
+      const int len = axis == 0 ? height : width;
+      if (len < 2) continue;
+      const int lines = axis == 0 ? width : height;
+      k_blur_lines<<<(lines + 63) / 64, 64, 0, s>>>(gray, width, height, axis, 9, b, d_f, vv);
+      const long long m = axis == 0 ? static_cast<long long>(height - 1) * width
+                                    : static_cast<long long>(height) * (width - 1);
+      if (pairwise_sum(d_f, m, sum_ptr, s) != RF_OK || pairwise_sum(vv, m, sum_ptr + 1, s) != RF_OK)
+        st = RF_CUDA;
+      sum_ptr += 2;
+      ++axes;
+    }
+    k_blur_finish<<<1, 1, 0, s>>>(sums, axes, blur_weight);
+  }
+  void* bufs[] = {b, d_f, vv, sums};
+  for (void* p : bufs)
+    if (p) cudaFreeAsync(p, s);
+  if (st != RF_OK) return st;
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_color_prep(const double* color, int32_t width, int32_t height,
+                        const double* gauss_weights, int32_t radius, double gain,
+                        double* member_color, double* blur_weight, void* stream) {
+  if (!color || !member_color || !blur_weight) return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* gray = nullptr;
+  if (cudaMallocAsync(&gray, sizeof(double) * width * height, s) != cudaSuccess) return RF_CUDA;
+  rf_status st = rf_unsharp_mask(color, width, height, 3, gauss_weights, radius, gain,
+                                 member_color, stream);
+  if (st == RF_OK) st = rf_grayscale(color, width, height, gray, stream);
+  if (st == RF_OK) st = rf_blurriness(gray, width, height, blur_weight, stream);
+  cudaFreeAsync(gray, s);
+  return st;
+}
+
+rf_status rf_fuse_color(const double* kf_depth, const double* kf_weight, int32_t width,
+                        int32_t height, double fx, double fy, double cx, double cy,
+                        int32_t n_members, const rf_member_view* members, double delta_occl,
+                        int32_t blas_order, double* kf_color, uint8_t* color_valid,
+                        void* stream) {
+  if (!kf_depth || !kf_weight || !kf_color || !color_valid || width <= 0 || height <= 0 ||
+      n_members < 0 || n_members > kMaxMembers || (n_members > 0 && !members))
+    return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<MemberDev> host(static_cast<size_t>(std::max(n_members, 1)));
+  for (int m = 0; m < n_members; ++m) {
+    if (!members[m].depth || !members[m].w_map || !members[m].color || !members[m].blur_weight)
+      return RF_INVALID_ARG;
+    host[m].depth = members[m].depth;
+    host[m].w_map = members[m].w_map;
+    host[m].color = members[m].color;
+    host[m].blur = members[m].blur_weight;
+    host[m].rel = members[m].rel;
+  }
+  MemberDev* d = nullptr;
+  if (cudaMallocAsync(&d, sizeof(MemberDev) * host.size(), s) != cudaSuccess) return RF_CUDA;
+  cudaMemcpyAsync(d, host.data(), sizeof(MemberDev) * host.size(), cudaMemcpyHostToDevice, s);
+  const int n = width * height;
+  k_fuse_color<<<(n + 127) / 128, 128, 0, s>>>(kf_depth, kf_weight,
+                                                make_intr(width, height, fx, fy, cx, cy), d,
+                                                n_members, delta_occl, blas_order, kf_color,
+                                                color_valid);
+  cudaFreeAsync(d, s);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+}  // extern "C"
