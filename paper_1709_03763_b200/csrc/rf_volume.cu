@@ -336,7 +336,9 @@ void memo_evict_lru(rf_volume* v) {
 // Returns the memo entry for (kf, pose) and whether it pre-existed.
 FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bool& existed) {
   existed = false;
-  if (v->memo_budget == 0) return nullptr;
+  // a shard's memo would hold only its own keys, but the contract check
+  // must see the whole footprint: sharded volumes sample every time
+  if (v->memo_budget == 0 || v->cfg.shard_count > 1) return nullptr;
   const MemoKey key = memo_key(kf, pose);
   auto it = v->memo.find(key);
   if (it != v->memo.end()) {
