@@ -68,6 +68,11 @@ typedef struct rf_kf_view {
     const double *color;   /* [height][width][3] device, or NULL (zeros, volume.py:256-259) */
     int32_t width, height;
     double fx, fy, cx, cy;
+    /* cudaEvent_t recorded after the planes' upload (e.g. on a copy stream),
+     * or NULL: the volume's stream waits on it before the first kernel that
+     * reads this keyframe, so host->device uploads overlap earlier entries'
+     * fusion inside one batched call. */
+    void *ready_event;
 } rf_kf_view;
 
 /* IntegrationRecord counts (src/refusion/volume.py:126-134). */
@@ -277,6 +282,14 @@ rf_status rf_fuse_color(const double *kf_depth, const double *kf_weight,
  * span [-exp_span, exp_span]; *mismatches = differing bit patterns. */
 rf_status rf_selftest_division(uint64_t n, uint64_t seed, int32_t exp_span,
                                uint64_t *mismatches);
+
+/* Compare the screened voxel projection (approximate reciprocal + exact
+ * fallback near pixel boundaries) with the exact IEEE projection on n
+ * random camera points around a width x height image with centre (cx, cy),
+ * half of them snapped within a few ulps of a pixel boundary;
+ * *mismatches = points whose pixel (or in/out decision) differs. */
+rf_status rf_selftest_projection(int32_t width, int32_t height, double cx, double cy,
+                                 uint64_t n, uint64_t seed, uint64_t *mismatches);
 
 /* ---- synthetic data (measurement infrastructure, synth.py:46-283) ------ */
 typedef struct rf_synth_prim {

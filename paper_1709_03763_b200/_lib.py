@@ -53,6 +53,7 @@ class RfKfView(ctypes.Structure):
         ("fy", ctypes.c_double),
         ("cx", ctypes.c_double),
         ("cy", ctypes.c_double),
+        ("ready_event", ctypes.c_void_p),
     ]
 
 
@@ -199,6 +200,9 @@ SIGNATURES = {
                          ctypes.c_int32, _vp, _vp, _vp]),
     "rf_selftest_division": (_S, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int32,
                                   ctypes.POINTER(ctypes.c_uint64)]),
+    "rf_selftest_projection": (_S, [ctypes.c_int32, ctypes.c_int32, ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
+                                    ctypes.POINTER(ctypes.c_uint64)]),
     "rf_set_memo_budget": (_S, [_vp, ctypes.c_int64]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),

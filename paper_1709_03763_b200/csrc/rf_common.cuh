@@ -110,6 +110,7 @@ struct Table {
   int* free_stack;
   int* returned;
   int* touched;   // slot | kNewFlag
+  long long* touched_keys;  // packed key of touched[i] (fuse reads no keys[] indirection)
   int* new_list;  // slots created by the current op
   long long* pend_tab;   // open-addressing set of keys to create (-1 = empty)
   long long* pend_keys;  // distinct pending keys of the current op

@@ -78,6 +78,8 @@ struct rf_volume {
   unsigned long long* d_u64 = nullptr;  // scratch counters [8]
   unsigned long long* h_u64 = nullptr;  // pinned [8]
   double* d_wsums = nullptr;
+  unsigned* d_gc_stamp = nullptr;  // per bucket: epoch of the GC that owns it
+  unsigned gc_epoch = 0;
   double* d_f64 = nullptr;
   double* h_f64 = nullptr;
   AllocState* h_alloc = nullptr;  // pinned
@@ -146,6 +148,17 @@ struct ProfScope {
     }
   }
 };
+
+// The fuse kernels stage their copies in > 48 KB of dynamic shared memory.
+void set_fuse_smem_attrs() {
+  cudaFuncSetAttribute(k_fuse<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse<kRemoveReadd>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse_single<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse_single<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+  cudaFuncSetAttribute(k_fuse_single<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+}
 
 KfView to_view(const rf_kf_view* kf) {
   KfView k;
@@ -237,8 +250,12 @@ void op_stream(Batch& b, const double c[3]) {
   p.op_index = op;
   p.op = v->d_ops + op;
   p.ws = v->d_ws;
-  k_stream<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, p);
-  if (v->profiling) v->prof_launches += 1;
+  // tiers are a function of the centre: an unchanged centre moves nothing
+  const bool same = b.has_center && c[0] == b.center[0] && c[1] == b.center[1] && c[2] == b.center[2];
+  if (!same) {
+    k_stream<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, p);
+    if (v->profiling) v->prof_launches += 1;
+  }
   // relocation (volume.py:358-364): centre moved more than one block span
   int reloc = 0;
   if (b.has_center) {
@@ -280,6 +297,12 @@ void set_dim_bits(FuseParams& p) {
   const double w = static_cast<double>(p.kf.width), h = static_cast<double>(p.kf.height);
   std::memcpy(&p.w_bits, &w, sizeof(w));
   std::memcpy(&p.h_bits, &h, sizeof(h));
+  // voxel-centre offsets (l + 0.5) * voxel_size (_kernels_cy.pyx:55-57)
+  for (int l = 0; l < 8; ++l) p.hz[l] = (static_cast<double>(l) + 0.5) * p.voxel_size;
+  // screened projection preconditions (rf_kernels.cuh, screen_coord)
+  const double lim = 16384.0;
+  p.fast_proj = p.kf.width < 16384 && p.kf.height < 16384 && std::fabs(p.kf.cx) < lim &&
+                std::fabs(p.kf.cy) < lim;
 }
 
 FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, int op) {
@@ -356,13 +379,12 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
     cudaGetLastError();
     return nullptr;
   }
-  FpEntry h{};
-  h.keys = reinterpret_cast<long long*>(static_cast<char*>(mem) + ((sizeof(FpEntry) + 15) & ~size_t(15)));
-  h.cap = cap;
-  h.valid = 0;
   FpEntry* dev = static_cast<FpEntry*>(mem);
-  // the descriptor is pageable host data: copy synchronously w.r.t. the host
-  cudaMemcpyAsync(dev, &h, sizeof(FpEntry), cudaMemcpyHostToDevice, v->stream);
+  // initialise the descriptor on the stream (a pageable host->device copy
+  // would synchronise the host with the stream mid-batch)
+  k_memo_init<<<1, 1, 0, v->stream>>>(
+      dev, reinterpret_cast<long long*>(static_cast<char*>(mem) + ((sizeof(FpEntry) + 15) & ~size_t(15))),
+      cap);
   v->memo_lru.push_front(key);
   MemoSlot slot;
   slot.dev = dev;
@@ -376,6 +398,7 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
 // mode: 0 integrate, 1 deintegrate, 2 allocate only
 void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
+  if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
@@ -408,21 +431,21 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   b.fparams.back().capture = nullptr;  // the fix-up relaunch must not re-capture
   if (mode == 2) {
     p.alloc_only = 1;
-    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
     if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
   if (mode == 0) {
     ProfScope ps(v, 0);
-    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, 0, v->stream>>>(v->T, p);
+    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
   } else {
     {
       ProfScope ps(v, 1);
-      k_fuse<kCheckRemove><<<v->fuse_grids[kCheckRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
+      k_fuse<kCheckRemove><<<v->fuse_grids[kCheckRemove], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
     }
     p.capture = nullptr;
     ProfScope ps(v, 0);
-    k_fuse<kApplyRemove><<<v->fuse_grids[kApplyRemove], kFuseThreads, 0, v->stream>>>(v->T, p);
+    k_fuse<kApplyRemove><<<v->fuse_grids[kApplyRemove], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
   }
   if (v->profiling) {
     v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
@@ -436,10 +459,13 @@ void op_gc(Batch& b) {
   b.infos.push_back({3, -1});
   b.fparams.emplace_back();
   b.gc_op = op;
-  const long long grid = std::min<long long>((v->cfg.hash_buckets + 255) / 256, v->n_sms * 8);
+  if (++v->gc_epoch == 0) {  // stamps wrapped: clear them
+    cudaMemsetAsync(v->d_gc_stamp, 0, sizeof(unsigned) * v->cfg.hash_buckets, v->stream);
+    v->gc_epoch = 1;
+  }
   // freed count lands in the op's n_new field
-  k_gc<<<static_cast<int>(std::max(1LL, grid)), 256, 0, v->stream>>>(
-      v->T, op, v->d_ws, &v->d_ops[op].n_new);
+  k_gc<<<v->n_sms * 8, 256, 0, v->stream>>>(v->T, op, v->d_ws, &v->d_ops[op].n_new,
+                                             v->d_gc_stamp, v->gc_epoch);
   if (v->profiling) v->prof_launches += 1;
 }
 
@@ -463,7 +489,7 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
     // volume.py:331-333: blocks sorted before the failing one were removed
     // and re-added; the rest stays untouched.  The later ops were skipped,
     // so the failed op's touched list is still intact.
-    k_fuse<kRemoveReadd><<<v->fuse_grids[kRemoveReadd], kFuseThreads, 0, v->stream>>>(v->T, b.fparams[out.err_op]);
+    k_fuse<kRemoveReadd><<<v->fuse_grids[kRemoveReadd], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, b.fparams[out.err_op]);
     RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
     RF_CUDA_TRY(v, cudaGetLastError());
   }
@@ -562,11 +588,20 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
     return RF_CUDA;
   }
   cudaDeviceGetAttribute(&v->n_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+  {  // the stream-ordered pool keeps what it has (memo entries, scratch): no
+     // OS-level unmap / map between batches
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cfg->device) == cudaSuccess) {
+      unsigned long long thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  }
+  set_fuse_smem_attrs();
   int occ[4] = {1, 1, 1, 1};
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, kFuseSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, kFuseSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, kFuseSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, kFuseSmemBytes);
   for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
@@ -585,6 +620,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
             alloc(reinterpret_cast<void**>(&T.free_stack), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.returned), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.touched), sizeof(int) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.touched_keys), sizeof(long long) * cap) &&
             alloc(reinterpret_cast<void**>(&T.new_list), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.pend_tab), sizeof(long long) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.pend_keys), sizeof(long long) * kPendingSlots) &&
@@ -593,6 +629,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
             alloc(reinterpret_cast<void**>(&T.alloc), sizeof(AllocState)) &&
             alloc(reinterpret_cast<void**>(&T.pool), sizeof(double) * kBlockDoubles * cap) &&
             alloc(reinterpret_cast<void**>(&v->d_ws), sizeof(WinState)) &&
+            alloc(reinterpret_cast<void**>(&v->d_gc_stamp), sizeof(unsigned) * cfg->hash_buckets) &&
             alloc(reinterpret_cast<void**>(&v->d_u64), sizeof(unsigned long long) * 8) &&
             alloc(reinterpret_cast<void**>(&v->d_f64), sizeof(double) * 8) &&
             cudaMallocHost(&v->h_ws, sizeof(WinState)) == cudaSuccess &&
@@ -607,6 +644,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   cudaMemset(T.keys, 0xff, sizeof(long long) * cap);
   cudaMemset(T.pend_tab, 0xff, sizeof(long long) * kPendingSlots);
   cudaMemset(T.nz, 0, sizeof(int) * cap);
+  cudaMemset(v->d_gc_stamp, 0, sizeof(unsigned) * cfg->hash_buckets);
   cudaMemset(T.stamp, 0, sizeof(unsigned) * cap);
   cudaMemset(T.alloc, 0, sizeof(AllocState));
   cudaMemset(v->d_ws, 0, sizeof(WinState));
@@ -623,8 +661,8 @@ rf_status rf_volume_destroy(rf_volume* v) {
   cudaSetDevice(v->cfg.device);
   cudaDeviceSynchronize();
   Table& T = v->T;
-  void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched,
-                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums};
+  void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched, T.touched_keys,
+                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums, v->d_gc_stamp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {v->h_ws, v->h_u64, v->h_f64, v->h_alloc, v->h_ops};
@@ -672,6 +710,7 @@ rf_status rf_footprint(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
   const long long npix = static_cast<long long>(kf->width) * kf->height;
+  if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
   FootprintParams p = footprint_params(v, b, kf, pose, 0);
   long long dcap = npix * 4 + 1024;
   for (int attempt = 0; attempt < 2; ++attempt) {
@@ -1047,6 +1086,7 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
             (!kf_color || cudaMalloc(&d_kc, sizeof(double) * 3 * npix) == cudaSuccess);
   rf_status st = RF_OK;
   if (ok) {
+    set_fuse_smem_attrs();
     cudaMemcpy(d_blk, blk.data(), sizeof(double) * kBlockDoubles, cudaMemcpyHostToDevice);
     cudaMemcpy(d_kd, kf_depth, sizeof(double) * npix, cudaMemcpyHostToDevice);
     cudaMemcpy(d_kw, kf_weight, sizeof(double) * npix, cudaMemcpyHostToDevice);
@@ -1071,14 +1111,14 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
     set_dim_bits(p);
     int cnt = 0;
     if (remove) {
-      k_fuse_single<kCheckRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+      k_fuse_single<kCheckRemove><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
       cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
       if (cnt == 0) {
-        k_fuse_single<kApplyRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+        k_fuse_single<kApplyRemove><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
         cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
       }
     } else {
-      k_fuse_single<kIntegrate><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt);
+      k_fuse_single<kIntegrate><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
       cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
     }
     if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -1111,6 +1151,29 @@ rf_status rf_selftest_division(uint64_t n, uint64_t seed, int32_t exp_span, uint
   if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return RF_CUDA;
   cudaMemset(d, 0, sizeof(unsigned long long));
   k_selftest_division<<<148 * 8, 256>>>(n, seed, exp_span, d);
+  unsigned long long h = 0;
+  cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  const cudaError_t e = cudaGetLastError();
+  cudaFree(d);
+  if (e != cudaSuccess) return RF_CUDA;
+  *mismatches = h;
+  return RF_OK;
+}
+
+rf_status rf_selftest_projection(int32_t width, int32_t height, double cx, double cy,
+                                 uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  if (!mismatches || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  FuseParams p{};
+  p.kf.width = width;
+  p.kf.height = height;
+  p.kf.cx = cx;
+  p.kf.cy = cy;
+  set_dim_bits(p);
+  if (!p.fast_proj) return RF_INVALID_ARG;
+  unsigned long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(unsigned long long)) != cudaSuccess) return RF_CUDA;
+  cudaMemset(d, 0, sizeof(unsigned long long));
+  k_selftest_projection<<<148 * 8, 256>>>(p, n, seed, d);
   unsigned long long h = 0;
   cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
   const cudaError_t e = cudaGetLastError();

@@ -155,6 +155,11 @@ def pose_struct(pose):
     return p
 
 
+def _is_device(arr, device):
+    torch = _torch()
+    return isinstance(arr, torch.Tensor) and arr.is_cuda and arr.device.index == device
+
+
 def _device_plane(arr, shape, device):
     """CUDA float64 contiguous tensor for a plane (numpy / torch input)."""
     torch = _torch()
@@ -167,27 +172,49 @@ def _device_plane(arr, shape, device):
         t = t.contiguous()
     else:
         a = np.ascontiguousarray(np.asarray(arr, dtype=np.float64))
-        t = torch.from_numpy(a).to(f"cuda:{device}")
+        t = torch.from_numpy(a).to(f"cuda:{device}", non_blocking=True)
     if tuple(t.shape) != tuple(shape):
         raise ValueError(f"keyframe plane shape {tuple(t.shape)} != {tuple(shape)}")
     return t
 
 
-def kf_view(kf, device=0):
-    """(rf_kf_view, keep-alive tensors) for a duck-typed keyframe."""
+def kf_view(kf, device=0, copy_stream=None):
+    """(rf_kf_view, keep-alive objects) for a duck-typed keyframe.
+
+    Planes already on the device are passed by pointer.  Host planes are
+    uploaded; with ``copy_stream`` the upload is issued there (pinned host
+    memory makes it asynchronous) and the view carries a ready event the
+    volume's stream waits on, so uploads overlap the fusion of earlier
+    entries of a batched call."""
+    torch = _torch()
     intr = kf.intrinsics
     h, w = int(intr.height), int(intr.width)
-    depth = _device_plane(kf.depth, (h, w), device)
-    weight = _device_plane(kf.weight, (h, w), device)
     color = getattr(kf, "color", None)
-    color_t = None if color is None else _device_plane(color, (h, w, 3), device)
+    planes = [(kf.depth, (h, w)), (kf.weight, (h, w))]
+    if color is not None:
+        planes.append((color, (h, w, 3)))
+    on_host = any(not _is_device(a, device) for a, _ in planes)
+    event = None
+    if on_host and copy_stream is not None:
+        consumer = torch.cuda.current_stream(device)
+        with torch.cuda.stream(copy_stream):
+            ts = [_device_plane(a, shp, device) for a, shp in planes]
+            event = torch.cuda.Event()
+            event.record(copy_stream)
+        for t in ts:
+            t.record_stream(consumer)
+    else:
+        ts = [_device_plane(a, shp, device) for a, shp in planes]
+    depth, weight = ts[0], ts[1]
+    color_t = ts[2] if color is not None else None
     v = L.RfKfView()
     v.depth = depth.data_ptr()
     v.weight = weight.data_ptr()
     v.color = color_t.data_ptr() if color_t is not None else None
     v.width, v.height = w, h
     v.fx, v.fy, v.cx, v.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
-    return v, (depth, weight, color_t)
+    v.ready_event = event.cuda_event if event is not None else None
+    return v, (depth, weight, color_t, event)
 
 
 # ---------------------------------------------------------------------------
@@ -251,6 +278,13 @@ class TwoTierStore:
             lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
             st = getattr(lib, name)(self._ptr, *args)
         _check(self._ptr, st, name)
+
+    def _copy_stream(self):
+        """Side stream for host->device keyframe uploads (created lazily)."""
+        if getattr(self, "_copy", None) is None:
+            torch = _torch()
+            self._copy = torch.cuda.Stream(device=self.device)
+        return self._copy
 
     def close(self):
         if self._ptr is not None:
@@ -515,8 +549,9 @@ def correct_windows(store, windows, cfg, next_center=None):
     news = (L.RfPose * n)()
     sizes = (ctypes.c_int32 * len(windows))(*[len(w) for w in windows])
     keep = []
+    copy_stream = store._copy_stream()
     for i, e in enumerate(entries):
-        v, k = kf_view(e.kf, store.device)
+        v, k = kf_view(e.kf, store.device, copy_stream)
         views[i] = v
         keep.append(k)
         olds[i] = pose_struct(e.integrated_pose)

@@ -282,3 +282,19 @@ def test_shared_denominator_division_is_ieee(exp_span):
     assert L.lib().rf_selftest_division(1 << 27, 1234 + exp_span, exp_span,
                                         ctypes.byref(bad)) == 0
     assert bad.value == 0
+
+
+@pytest.mark.parametrize("shape", [(640, 480, 319.5, 239.5), (1920, 1080, 959.25, 540.75),
+                                   (64, 48, 31.5, 23.5)])
+def test_screened_projection_is_exact(shape):
+    """The integrate kernels pick each voxel's pixel with an approximate
+    reciprocal and fall back to IEEE division within 2^-24 of a pixel
+    boundary; the pixel / in-image decision must equal the exact one."""
+    import ctypes
+
+    from paper_1709_03763_b200 import _lib as L
+
+    w, h, cx, cy = shape
+    bad = ctypes.c_uint64()
+    assert L.lib().rf_selftest_projection(w, h, cx, cy, 1 << 26, 77, ctypes.byref(bad)) == 0
+    assert bad.value == 0
