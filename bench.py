@@ -369,6 +369,7 @@ def run_b200(args):
                    "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MiB write, outside the step events)"},
         "gpu_launches": int(round(prof.kernel_launches * args.steps / prof_steps)),
+        "step_ms": [round(t, 3) for t in times],
         "host_select_ms_per_update": statistics.median(select_ms) if select_ms else None,
         "roofline": roof,
         "clocks": clk.summary(),

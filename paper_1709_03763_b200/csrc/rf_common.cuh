@@ -80,6 +80,11 @@ struct OpCounters {
   long long fail_key;                 // min key whose removal check failed
   int executed;                       // 1 once the op's first kernel ran
   int capacity;                       // 1 when the pool overflowed
+  // voxels a fuse kernel defers to its exact IEEE tail (operands outside
+  // the fast paths' exponent range), and the kernel's finished-CTA count;
+  // index 0 the removal check, 1 integrate / removal, 2 the fix-up
+  unsigned n_defer[3];
+  unsigned done_ctas[3];
 };
 
 // Allocator state (device).  Pops during one footprint kernel only read the
@@ -119,6 +124,8 @@ struct Table {
   long long* spill_keys; // tile keys that did not fit in shared memory
   int spill_cap;
   AllocState* alloc;
+  unsigned long long* defer;  // deferred voxels: slot << 10 | fresh << 9 | voxel
+  int defer_cap;
   long long buckets;
   int capacity;
 };
@@ -148,7 +155,13 @@ __device__ __forceinline__ unsigned lanemask_lt() {
   return m;
 }
 
-__device__ __forceinline__ double block_center_dist2_free(long long key, double span,
+// ||centre(b) - c||^2 summed as volume.py:345-346 does, (dx^2 + dy^2) + dz^2.
+// The reference compares sqrt of it with stream_radius; since the IEEE
+// square root is monotone, sqrt(x) <= R  <=>  x <= radius2 with radius2 the
+// largest double whose square root rounds to <= R (sqrt_le_bound, host),
+// so the kernels compare squared distances and never take a square root.
+
+__host__ __device__ __forceinline__ double block_center_dist2_free(long long key, double span,
                                                           const double* c) {
   long long bx, by, bz;
   unpack_key(key, bx, by, bz);
@@ -156,11 +169,6 @@ __device__ __forceinline__ double block_center_dist2_free(long long key, double 
   const double dy = (static_cast<double>(by) + 0.5) * span - c[1];
   const double dz = (static_cast<double>(bz) + 0.5) * span - c[2];
   return dx * dx + dy * dy + dz * dz;
-}
-
-// ||centre(b) - c|| as volume.py:345-346 computes it: sqrt((dx^2 + dy^2) + dz^2).
-__device__ __forceinline__ double block_center_dist(long long key, double span, const double* c) {
-  return sqrt(block_center_dist2_free(key, span, c));
 }
 
 }  // namespace rf

@@ -16,12 +16,14 @@
 #include <list>
 #include <unordered_map>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "refusion_b200.h"
 #include "rf_kernels.cuh"
+#include "rf_fuse_legacy.cuh"
 
 using namespace rf;
 
@@ -32,6 +34,7 @@ constexpr int kMaxWindowOps = 4096;
 constexpr int kPendingSlots = 1 << 20;
 // tile keys beyond a tile's shared-memory list (only pathological tiles)
 constexpr int kSpillSlots = 1 << 20;
+constexpr int kDeferSlots = 1 << 20;  // voxels a fuse kernel may defer to its exact tail
 
 struct EventPair {
   cudaEvent_t a, b;
@@ -59,8 +62,8 @@ struct MemoKeyHash {
 };
 
 struct MemoSlot {
-  FpEntry* dev = nullptr;  // descriptor + keys in one allocation
-  size_t bytes = 0;
+  FpEntry* dev = nullptr;  // descriptor + keys: one slot of the memo arena
+  int index = -1;
   std::list<MemoKey>::iterator lru;
 };
 
@@ -91,12 +94,20 @@ struct rf_volume {
   int n_sms = 148;
   int fuse_grid = 148 * 2;
   int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
+  int legacy_grids[4] = {148, 148, 148, 148};
+  bool legacy_fuse = false;  // RF_FUSE_IMPL=legacy: whole-block-prefetch A/B baseline
   int fp_grid_cap = 148 * 8;
   // footprint memo
   std::unordered_map<MemoKey, MemoSlot, MemoKeyHash> memo;
   std::list<MemoKey> memo_lru;
-  size_t memo_bytes = 0;
   size_t memo_budget = size_t(2) << 30;
+  // fixed-size slots carved from one allocation made at first use (no
+  // stream-ordered allocation inside a batch); keyframes needing more keys
+  // than a slot holds are not memoised
+  char* memo_arena = nullptr;
+  size_t memo_slot_bytes = 0;
+  int memo_slot_cap = 0;
+  std::vector<int> memo_free;
   // profiling
   bool profiling = false;
   std::vector<EventPair> events;
@@ -149,15 +160,13 @@ struct ProfScope {
   }
 };
 
-// The fuse kernels stage their copies in > 48 KB of dynamic shared memory.
-void set_fuse_smem_attrs() {
-  cudaFuncSetAttribute(k_fuse<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse<kRemoveReadd>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse_single<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse_single<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
-  cudaFuncSetAttribute(k_fuse_single<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFuseSmemBytes);
+// Largest double x with sqrt(x) <= r (IEEE sqrt, correctly rounded on host
+// and device alike): the squared-distance form of `dist <= r`.
+double sqrt_le_bound(double r) {
+  double x = r * r;
+  while (std::sqrt(x) > r) x = std::nextafter(x, 0.0);
+  while (std::sqrt(std::nextafter(x, INFINITY)) <= r) x = std::nextafter(x, INFINITY);
+  return x;
 }
 
 KfView to_view(const rf_kf_view* kf) {
@@ -246,7 +255,7 @@ void op_stream(Batch& b, const double c[3]) {
   std::memcpy(p.new_c, c, sizeof(p.new_c));
   p.has_old = b.has_center;
   p.span = kBlockSide * v->cfg.voxel_size;
-  p.radius = v->cfg.stream_radius;
+  p.radius2 = sqrt_le_bound(v->cfg.stream_radius);
   p.op_index = op;
   p.op = v->d_ops + op;
   p.ws = v->d_ws;
@@ -279,7 +288,7 @@ FootprintParams footprint_params(rf_volume* v, const Batch& b, const rf_kf_view*
   p.span = kBlockSide * v->cfg.voxel_size;
   p.inv_span = 1.0 / p.span;                       // volume.py:177
   p.min_z = 0.25 * v->cfg.voxel_size;              // volume.py:30, :170
-  p.radius = v->cfg.stream_radius;
+  p.radius2 = sqrt_le_bound(v->cfg.stream_radius);
   std::memcpy(p.center, b.center, sizeof(p.center));
   p.has_center = b.has_center;
   p.n_steps = static_cast<int>(std::ceil(2.0 * v->cfg.mu / v->cfg.voxel_size)) + 1;  // :172
@@ -349,11 +358,23 @@ void memo_evict_lru(rf_volume* v) {
   const MemoKey& old = v->memo_lru.back();
   auto it = v->memo.find(old);
   if (it != v->memo.end()) {
-    cudaFreeAsync(it->second.dev, v->stream);
-    v->memo_bytes -= it->second.bytes;
+    v->memo_free.push_back(it->second.index);
     v->memo.erase(it);
   }
   v->memo_lru.pop_back();
+}
+
+void memo_release(rf_volume* v) {
+  v->memo.clear();
+  v->memo_lru.clear();
+  v->memo_free.clear();
+  if (v->memo_arena) {
+    cudaDeviceSynchronize();  // kernels in flight may still read entries
+    cudaFree(v->memo_arena);
+  }
+  v->memo_arena = nullptr;
+  v->memo_slot_bytes = 0;
+  v->memo_slot_cap = 0;
 }
 
 // Returns the memo entry for (kf, pose) and whether it pre-existed.
@@ -371,28 +392,51 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
   }
   const long long npix = static_cast<long long>(kf->width) * kf->height;
   const int cap = static_cast<int>(std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
-  const size_t bytes = sizeof(FpEntry) + 16 + sizeof(long long) * static_cast<size_t>(cap);
-  if (bytes > v->memo_budget) return nullptr;
-  while (v->memo_bytes + bytes > v->memo_budget && !v->memo_lru.empty()) memo_evict_lru(v);
-  void* mem = nullptr;
-  if (cudaMallocAsync(&mem, bytes, v->stream) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
+  const size_t head = (sizeof(FpEntry) + 15) & ~size_t(15);
+  if (!v->memo_arena) {  // first use: slots sized for this keyframe
+    const size_t slot = (head + sizeof(long long) * static_cast<size_t>(cap) + 255) & ~size_t(255);
+    const size_t n = v->memo_budget / slot;
+    if (n == 0) return nullptr;
+    if (cudaMalloc(&v->memo_arena, n * slot) != cudaSuccess) {
+      cudaGetLastError();
+      v->memo_arena = nullptr;
+      v->memo_budget = 0;  // no memo on this device
+      return nullptr;
+    }
+    v->memo_slot_bytes = slot;
+    v->memo_slot_cap = cap;
+    v->memo_free.clear();
+    for (size_t i = n; i-- > 0;) v->memo_free.push_back(static_cast<int>(i));
   }
-  FpEntry* dev = static_cast<FpEntry*>(mem);
+  if (cap > v->memo_slot_cap) return nullptr;
+  if (v->memo_free.empty()) {
+    if (v->memo_lru.empty()) return nullptr;
+    memo_evict_lru(v);
+  }
+  const int index = v->memo_free.back();
+  v->memo_free.pop_back();
+  char* mem = v->memo_arena + static_cast<size_t>(index) * v->memo_slot_bytes;
+  FpEntry* dev = reinterpret_cast<FpEntry*>(mem);
   // initialise the descriptor on the stream (a pageable host->device copy
   // would synchronise the host with the stream mid-batch)
-  k_memo_init<<<1, 1, 0, v->stream>>>(
-      dev, reinterpret_cast<long long*>(static_cast<char*>(mem) + ((sizeof(FpEntry) + 15) & ~size_t(15))),
-      cap);
+  k_memo_init<<<1, 1, 0, v->stream>>>(dev, reinterpret_cast<long long*>(mem + head),
+                                      v->memo_slot_cap);
   v->memo_lru.push_front(key);
-  MemoSlot slot;
-  slot.dev = dev;
-  slot.bytes = bytes;
-  slot.lru = v->memo_lru.begin();
-  v->memo.emplace(key, slot);
-  v->memo_bytes += bytes;
+  MemoSlot ms;
+  ms.dev = dev;
+  ms.index = index;
+  ms.lru = v->memo_lru.begin();
+  v->memo.emplace(key, ms);
   return dev;
+}
+
+// Launch the batched fuse kernel of mode kMode (or the legacy A/B baseline).
+template <int kMode>
+void launch_fuse(rf_volume* v, const FuseParams& p) {
+  if (v->legacy_fuse)
+    k_fuse_legacy<kMode><<<v->legacy_grids[kMode], kFuseThreads, 0, v->stream>>>(v->T, p);
+  else
+    k_fuse<kMode><<<v->fuse_grids[kMode], kFuseThreads, 0, v->stream>>>(v->T, p);
 }
 
 // mode: 0 integrate, 1 deintegrate, 2 allocate only
@@ -409,7 +453,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     ProfScope ps(v, 2);
     if (memo) {
       const long long npix = static_cast<long long>(kf->width) * kf->height;
-      k_kf_hash<<<v->n_sms * 2, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
+      k_kf_hash<<<v->n_sms * 4, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
                                                       &v->d_ops[op].kf_hash);
       fp.kf_hash = &v->d_ops[op].kf_hash;
       fp.use_full = &v->d_ops[op].use_full;
@@ -431,21 +475,21 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   b.fparams.back().capture = nullptr;  // the fix-up relaunch must not re-capture
   if (mode == 2) {
     p.alloc_only = 1;
-    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
+    launch_fuse<kIntegrate>(v, p);
     if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
   if (mode == 0) {
     ProfScope ps(v, 0);
-    k_fuse<kIntegrate><<<v->fuse_grid, kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
+    launch_fuse<kIntegrate>(v, p);
   } else {
     {
       ProfScope ps(v, 1);
-      k_fuse<kCheckRemove><<<v->fuse_grids[kCheckRemove], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
+      launch_fuse<kCheckRemove>(v, p);
     }
     p.capture = nullptr;
     ProfScope ps(v, 0);
-    k_fuse<kApplyRemove><<<v->fuse_grids[kApplyRemove], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, p);
+    launch_fuse<kApplyRemove>(v, p);
   }
   if (v->profiling) {
     v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
@@ -489,7 +533,7 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
     // volume.py:331-333: blocks sorted before the failing one were removed
     // and re-added; the rest stays untouched.  The later ops were skipped,
     // so the failed op's touched list is still intact.
-    k_fuse<kRemoveReadd><<<v->fuse_grids[kRemoveReadd], kFuseThreads, kFuseSmemBytes, v->stream>>>(v->T, b.fparams[out.err_op]);
+    launch_fuse<kRemoveReadd>(v, b.fparams[out.err_op]);
     RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
     RF_CUDA_TRY(v, cudaGetLastError());
   }
@@ -596,13 +640,21 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
   }
-  set_fuse_smem_attrs();
   int occ[4] = {1, 1, 1, 1};
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, kFuseSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, kFuseSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, kFuseSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, kFuseSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, 0);
   for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse_legacy<kIntegrate>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse_legacy<kCheckRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse_legacy<kApplyRemove>, kFuseThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse_legacy<kRemoveReadd>, kFuseThreads, 0);
+  for (int m = 0; m < 4; ++m) v->legacy_grids[m] = v->n_sms * std::max(occ[m], 1);
+  {
+    const char* impl = std::getenv("RF_FUSE_IMPL");
+    v->legacy_fuse = impl && std::string(impl) == "legacy";
+  }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
   const size_t cap = static_cast<size_t>(cfg->block_capacity);
@@ -611,6 +663,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   T.capacity = static_cast<int>(cap);
   T.pend_mask = kPendingSlots - 1;
   T.spill_cap = kSpillSlots;
+  T.defer_cap = kDeferSlots;
   auto alloc = [&](void** p, size_t bytes) { return cudaMalloc(p, bytes) == cudaSuccess; };
   bool ok = alloc(reinterpret_cast<void**>(&T.heads), sizeof(int) * cfg->hash_buckets) &&
             alloc(reinterpret_cast<void**>(&T.keys), sizeof(long long) * cap) &&
@@ -626,6 +679,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
             alloc(reinterpret_cast<void**>(&T.pend_keys), sizeof(long long) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.pend_idx), sizeof(int) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.spill_keys), sizeof(long long) * kSpillSlots) &&
+            alloc(reinterpret_cast<void**>(&T.defer), sizeof(unsigned long long) * kDeferSlots) &&
             alloc(reinterpret_cast<void**>(&T.alloc), sizeof(AllocState)) &&
             alloc(reinterpret_cast<void**>(&T.pool), sizeof(double) * kBlockDoubles * cap) &&
             alloc(reinterpret_cast<void**>(&v->d_ws), sizeof(WinState)) &&
@@ -662,7 +716,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
   cudaDeviceSynchronize();
   Table& T = v->T;
   void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched, T.touched_keys,
-                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums, v->d_gc_stamp};
+                  T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.defer, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums, v->d_gc_stamp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   void* hptrs[] = {v->h_ws, v->h_u64, v->h_f64, v->h_alloc, v->h_ops};
@@ -673,7 +727,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
     cudaEventDestroy(e.b);
   }
   for (auto e : v->event_pool) cudaEventDestroy(e);
-  for (auto& kv : v->memo) cudaFree(kv.second.dev);
+  memo_release(v);
   delete v;
   return RF_OK;
 }
@@ -944,7 +998,8 @@ rf_status rf_counters_get(rf_volume* v, rf_counters* out) {
     k_count_active<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, v->center[0], v->center[1],
                                                         v->center[2],
                                                         kBlockSide * v->cfg.voxel_size,
-                                                        v->cfg.stream_radius, v->d_u64);
+                                                        sqrt_le_bound(v->cfg.stream_radius),
+                                                        v->d_u64);
   cudaMemcpyAsync(v->h_alloc, v->T.alloc, sizeof(AllocState), cudaMemcpyDeviceToHost, v->stream);
   cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                   v->stream);
@@ -1079,14 +1134,15 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
   }
   double *d_blk = nullptr, *d_kd = nullptr, *d_kw = nullptr, *d_kc = nullptr;
   int* d_cnt = nullptr;
-  bool ok = cudaMalloc(&d_blk, sizeof(double) * kBlockDoubles) == cudaSuccess &&
+  unsigned long long* d_def = nullptr;  // deferred-voxel list + count (512 + 1 entries)
+  bool ok = cudaMalloc(&d_def, sizeof(unsigned long long) * (kBlockVoxels + 1)) == cudaSuccess &&
+            cudaMalloc(&d_blk, sizeof(double) * kBlockDoubles) == cudaSuccess &&
             cudaMalloc(&d_kd, sizeof(double) * npix) == cudaSuccess &&
             cudaMalloc(&d_kw, sizeof(double) * npix) == cudaSuccess &&
             cudaMalloc(&d_cnt, sizeof(int)) == cudaSuccess &&
             (!kf_color || cudaMalloc(&d_kc, sizeof(double) * 3 * npix) == cudaSuccess);
   rf_status st = RF_OK;
   if (ok) {
-    set_fuse_smem_attrs();
     cudaMemcpy(d_blk, blk.data(), sizeof(double) * kBlockDoubles, cudaMemcpyHostToDevice);
     cudaMemcpy(d_kd, kf_depth, sizeof(double) * npix, cudaMemcpyHostToDevice);
     cudaMemcpy(d_kw, kf_weight, sizeof(double) * npix, cudaMemcpyHostToDevice);
@@ -1110,15 +1166,21 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
     p.eps_w = eps_w;
     set_dim_bits(p);
     int cnt = 0;
+    unsigned* d_defn = reinterpret_cast<unsigned*>(d_def + kBlockVoxels);
+    cudaMemset(d_defn, 0, sizeof(unsigned));
     if (remove) {
-      k_fuse_single<kCheckRemove><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
+      k_fuse_single<kCheckRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt,
+                                                                        d_def, d_defn);
       cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
       if (cnt == 0) {
-        k_fuse_single<kApplyRemove><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
+        cudaMemset(d_defn, 0, sizeof(unsigned));
+        k_fuse_single<kApplyRemove><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz,
+                                                                          d_cnt, d_def, d_defn);
         cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
       }
     } else {
-      k_fuse_single<kIntegrate><<<1, kFuseThreads, kFuseSmemBytes>>>(p, d_blk, ox, oy, oz, d_cnt);
+      k_fuse_single<kIntegrate><<<1, kFuseThreads>>>(p, d_blk, ox, oy, oz, d_cnt,
+                                                                      d_def, d_defn);
       cudaMemcpy(&cnt, d_cnt, sizeof(int), cudaMemcpyDeviceToHost);
     }
     if (cudaDeviceSynchronize() != cudaSuccess || cudaGetLastError() != cudaSuccess) {
@@ -1137,6 +1199,7 @@ rf_status rf_fuse_block(double* d, double* w, double* c, double ox, double oy, d
   } else {
     st = RF_CUDA;
   }
+  cudaFree(d_def);
   cudaFree(d_blk);
   cudaFree(d_kd);
   cudaFree(d_kw);
@@ -1186,8 +1249,8 @@ rf_status rf_selftest_projection(int32_t width, int32_t height, double cx, doubl
 rf_status rf_set_memo_budget(rf_volume* v, int64_t bytes) {
   if (!v || bytes < 0) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
+  memo_release(v);  // slots are re-carved for the new budget at next use
   v->memo_budget = static_cast<size_t>(bytes);
-  while (v->memo_bytes > v->memo_budget && !v->memo_lru.empty()) memo_evict_lru(v);
   return RF_OK;
 }
 

@@ -298,3 +298,37 @@ def test_screened_projection_is_exact(shape):
     bad = ctypes.c_uint64()
     assert L.lib().rf_selftest_projection(w, h, cx, cy, 1 << 26, 77, ctypes.byref(bad)) == 0
     assert bad.value == 0
+
+
+def test_extreme_values_take_the_exact_tail(V):
+    """Voxels whose update operands leave the fast paths' exponent range
+    (here colours ~1e305 / 1e-310 written into blocks) are re-fused by the
+    kernels' exact IEEE tail: results stay bit-identical to the oracle for
+    integration, the removal check and the removal."""
+    rng = np.random.default_rng(5)
+    cfg = V.VolumeConfig(voxel_size=0.01, mu=0.06, stream_radius=6.0, hash_buckets=1 << 16)
+    pose = S.SPose(S.rot_z(0.2) @ S.rot_y(0.05), [0.1, 0.05, 0.2])
+    f0, f1 = _vga_frame(rng), _vga_frame(rng, z=1.55, tilt=0.05)
+    store = V.TwoTierStore(block_capacity=1 << 15)
+    ref = O.OracleStore(cfg.voxel_size, cfg.mu, cfg.stream_radius)
+    V.stream(store, pose.translation, cfg)
+    ref.stream(pose.translation)
+    V.integrate(store, f0, pose, cfg)
+    ref.integrate(f0, pose)
+    keys, d, w, c = ref.export()
+    coords = O.keys_to_coords(keys)
+    pick = rng.choice(len(coords), size=min(40, len(coords)), replace=False)
+    for j in pick:
+        b = ref.find(coords[j])
+        vox = rng.choice(512, size=64, replace=False)
+        b.c[vox[:32], 0] = 1e305
+        b.c[vox[32:], 2] = 1e-310
+        store.put_block(coords[j], b.d.copy(), b.w.copy(), b.c.copy())
+    assert_same_state(store, ref)
+    rec = V.integrate(store, f1, pose, cfg)
+    _, touched, updated = ref.integrate(f1, pose)
+    assert (rec.blocks_touched, rec.voxels_updated) == (touched, updated)
+    assert_same_state(store, ref)
+    V.deintegrate(store, f0, pose, cfg)
+    ref.deintegrate(f0, pose)
+    assert_same_state(store, ref)

@@ -1,9 +1,13 @@
 """Small fixed workload for ncu captures (one GPU): build a corridor volume
 from --build keyframes, then run --corrections single-keyframe corrections.
-Kernel launch order: build = (reset, stream, footprint, commit, fuse<0>) x N,
-then per correction (reset, stream x2, footprint, commit, fuse<1>, fuse<2>,
-stream x2, footprint, commit, fuse<0>, gc, stream)."""
+Kernel launch order per correction: reset, stream, (kf_hash, cached) or
+footprint, spill, commit, k_fuse<1> (removal check), k_fuse<2> (removal),
+stream, kf_hash, footprint, spill, commit, k_fuse<0> (integrate), gc,
+stream.  --json writes the corrections' algorithmic bytes per fuse launch
+(80 B x voxels_updated + 40 B x H*W, the bench's roofline model) so an ncu
+capture of the same launches can be set beside them (tools/ncu_traffic.py)."""
 import argparse
+import json
 import os
 import sys
 
@@ -12,6 +16,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from paper_1709_03763_b200 import _lib as L  # noqa: E402
 from paper_1709_03763_b200 import reintegration as R  # noqa: E402
 from paper_1709_03763_b200 import synth as SY  # noqa: E402
 from paper_1709_03763_b200 import volume as V  # noqa: E402
@@ -20,6 +25,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--build", type=int, default=20)
 ap.add_argument("--corrections", type=int, default=2)
 ap.add_argument("--voxel", type=float, default=bench.VOXEL)
+ap.add_argument("--json", default=None)
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
@@ -33,9 +39,21 @@ for kf, p in zip(kfs, drifted):
     V.stream(store, p.translation, cfg)
     V.integrate(store, kf, p, cfg)
 torch.cuda.synchronize()
+lib = L.lib()
+lib.rf_profile_begin(store._ptr)
 for i in range(a.corrections):
     e = R.LedgerEntry(kfs[i], -1, drifted[i], gt_kf[i], 0, gt_kf[i])
     V.correct_entries(store, [e], cfg, next_center=gt_kf[i].translation)
     drifted[i] = gt_kf[i]
 torch.cuda.synchronize()
-print("blocks", store.block_count())
+prof = L.RfProfile()
+lib.rf_profile_end(store._ptr, L.ctypes.byref(prof))
+out = {"blocks": store.block_count(), "corrections": a.corrections,
+       "fuse_launches": int(prof.fuse_launches), "voxels_updated": int(prof.voxels_updated),
+       "blocks_touched": int(prof.blocks_touched),
+       "alg_bytes_per_fuse_launch": (80.0 * prof.voxels_updated + 40.0 * prof.pixels)
+       / max(prof.fuse_launches, 1),
+       "fuse_us_per_launch_events": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1)}
+print(json.dumps(out))
+if a.json:
+    json.dump(out, open(a.json, "w"), indent=1)
