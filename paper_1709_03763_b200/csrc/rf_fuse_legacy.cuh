@@ -190,7 +190,7 @@ __device__ __forceinline__ void bulk_prefetch_block(const Table& T, const double
                                                     unsigned bytes) {
   const unsigned entry = static_cast<unsigned>(__ldg(&T.touched[j]));
   if (entry & kNewFlag) return;
-  const double* src = base + static_cast<size_t>(entry & ~kNewFlag) * kBlockDoubles;
+  const double* src = base + static_cast<size_t>(entry & kSlotMask) * kBlockDoubles;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kFuseThreads, kMode == kCheckRemove ? 5 : 4)
     const int cap = p.capture->cap;
     if (n <= cap) {
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-        p.capture->keys[i] = T.keys[static_cast<unsigned>(T.touched[i]) & ~kNewFlag];
+        p.capture->keys[i] = T.keys[static_cast<unsigned>(T.touched[i]) & kSlotMask];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       p.capture->count = n;
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kFuseThreads, kMode == kCheckRemove ? 5 : 4)
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
       const unsigned entry = static_cast<unsigned>(T.touched[i]);
       if (!(entry & kNewFlag)) continue;
-      double* blk = T.pool + static_cast<size_t>(entry & ~kNewFlag) * kBlockDoubles;
+      double* blk = T.pool + static_cast<size_t>(entry & kSlotMask) * kBlockDoubles;
       for (int j = threadIdx.x; j < kBlockDoubles; j += blockDim.x) blk[j] = 0.0;
     }
     return;
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(kFuseThreads, kMode == kCheckRemove ? 5 : 4)
     if (slice == 0 && lane == 0 && i + static_cast<int>(gridDim.x) < n)
       bulk_prefetch_block(T, prefetch_base, i + gridDim.x, kPrefetchBytes);
     const unsigned entry = static_cast<unsigned>(__ldg(&T.touched[i]));
-    const int slot = static_cast<int>(entry & ~kNewFlag);
+    const int slot = static_cast<int>(entry & kSlotMask);
     const bool fresh = (entry & kNewFlag) != 0;
     const long long key = __ldg(&T.keys[slot]);
     double* blk = T.pool + static_cast<size_t>(slot) * kBlockDoubles;

@@ -96,6 +96,8 @@ struct rf_volume {
   int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
   int legacy_grids[4] = {148, 148, 148, 148};
   bool legacy_fuse = false;  // RF_FUSE_IMPL=legacy: whole-block-prefetch A/B baseline
+  int merged_grid = 148;
+  bool merge_pairs = false;  // RF_MERGE_PAIRS=1 enables k_fuse_merged
   int fp_grid_cap = 148 * 8;
   // footprint memo
   std::unordered_map<MemoKey, MemoSlot, MemoKeyHash> memo;
@@ -199,6 +201,7 @@ struct OpInfo {
   int kind;  // 0 stream, 1 integrate, 2 deintegrate, 3 gc, 4 allocate
   int entry;
   int window = 0;
+  bool merged = false;  // fused by k_fuse_merged with its neighbour
 };
 
 struct Batch {
@@ -211,6 +214,11 @@ struct Batch {
   std::vector<OpInfo> infos;
   std::vector<FuseParams> fparams;  // per op (fuse ops only)
   int gc_op = -1;
+  // a de-integration whose removal is deferred into the next integration's
+  // merged kernel (op index, its params and footprint epoch)
+  int pending_rm = -1;
+  FuseParams pending_p{};
+  unsigned pending_epoch = 0;
 };
 
 rf_status ensure_ops(rf_volume* v, int n) {
@@ -439,13 +447,23 @@ void launch_fuse(rf_volume* v, const FuseParams& p) {
     k_fuse<kMode><<<v->fuse_grids[kMode], kFuseThreads, 0, v->stream>>>(v->T, p);
 }
 
-// mode: 0 integrate, 1 deintegrate, 2 allocate only
-void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
+// mode: 0 integrate, 1 deintegrate, 2 allocate only.  defer_removal (mode
+// 1): run the removal check now but leave the removal to the next op, which
+// must be an integration called with merge = true: the two become one
+// k_fuse_merged launch over the union of their footprints (the stream ops
+// between them move no data, so per voxel the order is unchanged).
+void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry,
+             bool defer_removal = false, bool merge = false) {
   rf_volume* v = b.v;
   if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
+  merge = merge && mode == 0 && b.pending_rm >= 0;
+  if (merge) {
+    fp.merge_op = v->d_ops + b.pending_rm;
+    fp.merge_epoch = b.pending_epoch;
+  }
   bool existed = false;
   FpEntry* memo = memo_lookup(v, kf, pose, existed);
   int launches = 0;
@@ -473,32 +491,60 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   p.capture = memo;
   b.fparams.push_back(p);
   b.fparams.back().capture = nullptr;  // the fix-up relaunch must not re-capture
+  if (v->profiling) v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
   if (mode == 2) {
     p.alloc_only = 1;
     launch_fuse<kIntegrate>(v, p);
     if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
-  if (mode == 0) {
+  if (mode == 0 && merge) {
+    {
+      ProfScope ps(v, 0);
+      k_fuse_merged<<<v->merged_grid, kFuseThreads, kMergedSmemBytes, v->stream>>>(
+          v->T, b.pending_p, p);
+    }
+    b.infos[b.pending_rm].merged = true;
+    b.infos[op].merged = true;
+    b.pending_rm = -1;
+    launches += 1;
+  } else if (mode == 0) {
     ProfScope ps(v, 0);
     launch_fuse<kIntegrate>(v, p);
+    launches += 1;
   } else {
     {
       ProfScope ps(v, 1);
       launch_fuse<kCheckRemove>(v, p);
     }
     p.capture = nullptr;
-    ProfScope ps(v, 0);
-    launch_fuse<kApplyRemove>(v, p);
+    launches += 1;
+    if (defer_removal && v->merge_pairs && !v->legacy_fuse) {
+      b.pending_rm = op;
+      b.pending_p = p;
+      b.pending_epoch = fp.epoch;
+    } else {
+      ProfScope ps(v, 0);
+      launch_fuse<kApplyRemove>(v, p);
+      launches += 1;
+    }
   }
-  if (v->profiling) {
-    v->prof_pixels += static_cast<long long>(kf->width) * kf->height;
-    v->prof_launches += launches + (mode == 1 ? 2 : 1);
-  }
+  if (v->profiling) v->prof_launches += launches;
+}
+
+// A deferred removal whose integration never came (not produced by the
+// callers, kept for safety): run it on its own.
+void flush_pending(Batch& b) {
+  if (b.pending_rm < 0) return;
+  rf_volume* v = b.v;
+  ProfScope ps(v, 0);
+  launch_fuse<kApplyRemove>(v, b.pending_p);
+  b.pending_rm = -1;
 }
 
 void op_gc(Batch& b) {
   rf_volume* v = b.v;
+  flush_pending(b);
   const int op = next_op(b);
   b.infos.push_back({3, -1});
   b.fparams.emplace_back();
@@ -522,6 +568,7 @@ struct BatchOutcome {
 // the ops that executed.
 rf_status batch_end(Batch& b, BatchOutcome& out) {
   rf_volume* v = b.v;
+  flush_pending(b);
   const int n = std::max(b.n_ops, 1);
   cudaMemcpyAsync(v->h_ops, v->d_ops, sizeof(OpCounters) * n, cudaMemcpyDeviceToHost, v->stream);
   cudaMemcpyAsync(v->h_ws, v->d_ws, sizeof(WinState), cudaMemcpyDeviceToHost, v->stream);
@@ -547,8 +594,11 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
     for (int i = 0; i < b.n_ops; ++i) {
       const int k = b.infos[i].kind;
       if ((k == 1 || k == 2) && (!out.err_kind || i < out.err_op)) {
-        v->prof_voxels += static_cast<long long>(v->h_ops[i].voxels_updated);
-        v->prof_blocks += static_cast<long long>(v->h_ops[i].n_touched);
+        // a merged pair moves each voxel of the union once
+        const OpCounters& o = v->h_ops[i];
+        if (!b.infos[i].merged) v->prof_voxels += static_cast<long long>(o.voxels_updated);
+        else if (k == 1) v->prof_voxels += static_cast<long long>(o.voxels_union);
+        v->prof_blocks += static_cast<long long>(o.n_touched + (k == 1 ? o.n_shared : 0));
       }
     }
   }
@@ -622,7 +672,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   if (!(cfg->voxel_size > 0.0) || !(cfg->mu >= 2.0 * cfg->voxel_size) ||
       !(cfg->stream_radius > cfg->mu) || cfg->hash_buckets <= 0 ||
       cfg->hash_buckets > 0x7fffffffLL || cfg->block_capacity <= 0 ||
-      cfg->block_capacity > 0x7ffffff0LL || cfg->shard_count < 1 || cfg->shard_rank < 0 ||
+      cfg->block_capacity > 0x3ffffff0LL || cfg->shard_count < 1 || cfg->shard_rank < 0 ||
       cfg->shard_rank >= cfg->shard_count)
     return RF_INVALID_ARG;
   rf_volume* v = new rf_volume();
@@ -651,9 +701,14 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse_legacy<kApplyRemove>, kFuseThreads, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse_legacy<kRemoveReadd>, kFuseThreads, 0);
   for (int m = 0; m < 4; ++m) v->legacy_grids[m] = v->n_sms * std::max(occ[m], 1);
+  cudaFuncSetAttribute(k_fuse_merged, cudaFuncAttributeMaxDynamicSharedMemorySize, kMergedSmemBytes);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse_merged, kFuseThreads, kMergedSmemBytes);
+  v->merged_grid = v->n_sms * std::max(occ[0], 1);
   {
     const char* impl = std::getenv("RF_FUSE_IMPL");
     v->legacy_fuse = impl && std::string(impl) == "legacy";
+    const char* mp = std::getenv("RF_MERGE_PAIRS");
+    v->merge_pairs = mp && std::string(mp) == "1";
   }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
@@ -674,6 +729,7 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
             alloc(reinterpret_cast<void**>(&T.returned), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.touched), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.touched_keys), sizeof(long long) * cap) &&
+            alloc(reinterpret_cast<void**>(&T.tpos), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.new_list), sizeof(int) * cap) &&
             alloc(reinterpret_cast<void**>(&T.pend_tab), sizeof(long long) * kPendingSlots) &&
             alloc(reinterpret_cast<void**>(&T.pend_keys), sizeof(long long) * kPendingSlots) &&
@@ -715,7 +771,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
   cudaSetDevice(v->cfg.device);
   cudaDeviceSynchronize();
   Table& T = v->T;
-  void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched, T.touched_keys,
+  void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched, T.touched_keys, T.tpos,
                   T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.defer, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums, v->d_gc_stamp};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -889,13 +945,14 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     op_stream(b, o[0].t);
     for (int i = 0; i < m; ++i) {
       op_stream(b, o[i].t);
-      op_fuse(b, &k[i], &o[i], 1, i);
+      // the window's last removal merges with its first integration
+      op_fuse(b, &k[i], &o[i], 1, i, /*defer_removal=*/i == m - 1);
       b.infos.back().window = w;
     }
     op_stream(b, n[0].t);
     for (int i = 0; i < m; ++i) {
       op_stream(b, n[i].t);
-      op_fuse(b, &k[i], &n[i], 0, i);
+      op_fuse(b, &k[i], &n[i], 0, i, false, /*merge=*/i == 0);
       b.infos.back().window = w;
     }
     op_gc(b);
@@ -910,7 +967,8 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     if (out.err_kind && i > out.err_op) break;
     const OpInfo& inf = b.infos[i];
     if (inf.kind == 1 || inf.kind == 2) {
-      r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched);
+      r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched +
+                                               (inf.kind == 1 ? v->h_ops[i].n_shared : 0));
       r.n_new += static_cast<int64_t>(v->h_ops[i].n_new);
       if (inf.kind == 1) r.voxels_updated += static_cast<int64_t>(v->h_ops[i].voxels_updated);
     } else if (inf.kind == 3) {

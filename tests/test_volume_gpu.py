@@ -332,3 +332,101 @@ def test_extreme_values_take_the_exact_tail(V):
     V.deintegrate(store, f0, pose, cfg)
     ref.deintegrate(f0, pose)
     assert_same_state(store, ref)
+
+
+def _contract_window_case(cfg, rng):
+    """Search (with the oracle) a keyframe + (old, new) pose pair whose
+    re-integration fails the streaming contract on the INTEGRATION while the
+    removal succeeds: footprint blocks near the sphere's rim quantise in or
+    out with the pose."""
+    for _ in range(400):
+        f = S.random_frame(rng, z_lo=0.92, z_hi=1.02)
+        old = S.SPose(S.rot_y(rng.uniform(-0.3, 0.3)) @ S.rot_x(rng.uniform(-0.3, 0.3)),
+                      rng.uniform(-0.02, 0.02, 3))
+        new = S.SPose(old.rotation @ S.rot_z(rng.uniform(-0.3, 0.3)),
+                      old.translation + rng.uniform(-0.03, 0.03, 3))
+        ref = O.OracleStore(cfg.voxel_size, cfg.mu, cfg.stream_radius)
+        try:
+            ref.stream(old.translation)
+            ref.integrate(f, old)
+            ref.stream(old.translation)
+            ref.deintegrate(f, old)
+        except O.OracleError:
+            continue
+        try:
+            ref.stream(new.translation)
+            ref.integrate(f, new)
+        except O.StreamingContractError:
+            return f, old, new
+    pytest.skip("no rim case found")
+
+
+def test_window_integration_contract_error_matches_oracle(V):
+    """A window whose integration violates the streaming contract after its
+    removal succeeded (the pair runs as one merged removal + integration
+    kernel): the removal completes, the integration keeps its sorted-prefix
+    partial allocation, the error is StreamingContractError -- the state of
+    the reference's sequential _correct_entries."""
+    from paper_1709_03763_b200.errors import StreamingContractError
+
+    rng = np.random.default_rng(91)
+    cfg = V.VolumeConfig(voxel_size=0.01, mu=0.06, stream_radius=1.25, hash_buckets=1 << 14)
+    f, old, new = _contract_window_case(cfg, rng)
+    other = S.random_frame(rng, z_lo=0.5, z_hi=0.7)
+    store = V.TwoTierStore(block_capacity=1 << 14)
+    ref = O.OracleStore(cfg.voxel_size, cfg.mu, cfg.stream_radius)
+    for kf, p in ((other, old), (f, old)):
+        V.stream(store, p.translation, cfg)
+        V.integrate(store, kf, p, cfg)
+        ref.stream(p.translation)
+        ref.integrate(kf, p)
+    ents = [S.Entry(f, old.copy(), new.copy())]
+    rents = [S.Entry(f, old.copy(), new.copy())]
+    with pytest.raises(StreamingContractError):
+        V.correct_entries(store, ents, cfg)
+    with pytest.raises(O.StreamingContractError):
+        ref.correct_entries(rents)
+    assert_same_state(store, ref)
+
+
+@pytest.fixture()
+def merged_pairs(monkeypatch):
+    """Volumes created under this fixture run each window's last removal and
+    first integration as one k_fuse_merged launch (RF_MERGE_PAIRS=1)."""
+    monkeypatch.setenv("RF_MERGE_PAIRS", "1")
+
+
+def test_merged_pairs_window_bitexact(V, merged_pairs):
+    test_vga_window_correction_bitexact(V)
+
+
+def test_merged_pairs_contract_error(V, merged_pairs):
+    test_window_integration_contract_error_matches_oracle(V)
+
+
+def test_merged_pairs_extreme_values(V, merged_pairs):
+    """Deferred voxels of the merged kernel: both parts (removal, then
+    integration) re-fused by its exact tail."""
+    rng = np.random.default_rng(6)
+    cfg = V.VolumeConfig(voxel_size=0.01, mu=0.06, stream_radius=6.0, hash_buckets=1 << 16)
+    old = S.SPose(S.rot_z(0.2) @ S.rot_y(0.05), [0.1, 0.05, 0.2])
+    new = S.SPose(S.rot_z(0.21) @ S.rot_y(0.06), [0.11, 0.04, 0.21])
+    f0 = _vga_frame(rng)
+    store = V.TwoTierStore(block_capacity=1 << 15)
+    ref = O.OracleStore(cfg.voxel_size, cfg.mu, cfg.stream_radius)
+    V.stream(store, old.translation, cfg)
+    ref.stream(old.translation)
+    V.integrate(store, f0, old, cfg)
+    ref.integrate(f0, old)
+    keys, d, w, c = ref.export()
+    coords = O.keys_to_coords(keys)
+    for j in rng.choice(len(coords), size=min(40, len(coords)), replace=False):
+        b = ref.find(coords[j])
+        vox = rng.choice(512, size=64, replace=False)
+        b.c[vox, 1] = 1e305
+        store.put_block(coords[j], b.d.copy(), b.w.copy(), b.c.copy())
+    ents = [S.Entry(f0, old.copy(), new.copy())]
+    rents = [S.Entry(f0, old.copy(), new.copy())]
+    assert V.correct_entries(store, ents, cfg) == 1
+    ref.correct_entries(rents)
+    assert_same_state(store, ref)

@@ -35,7 +35,7 @@ nbytes = 10 * 640 * 480 * 32
 print(f"H2D depth+colour of 10 KF: {nbytes / dt / 1e9:.1f} GB/s ({1e3 * dt:.2f} ms)")
 cfg = V.VolumeConfig(voxel_size=bench.VOXEL, mu=bench.MU, stream_radius=bench.RADIUS,
                      hash_buckets=1 << 21)
-store = V.TwoTierStore(block_capacity=600_000)
+store = V.TwoTierStore(block_capacity=2_000_000)
 for kf, p in zip(kfs, dr):
     V.stream(store, p.translation, cfg)
     V.integrate(store, kf, p, cfg)
