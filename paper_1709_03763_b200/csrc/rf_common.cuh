@@ -96,6 +96,7 @@ struct OpCounters {
   unsigned long long voxels_union;
   unsigned capture_n;  // merged kernel: memo keys written so far
   unsigned next_block[3];  // fuse kernels: dynamic block queue (per defer index)
+  unsigned fp_done;        // footprint kernel: finished CTAs
 };
 
 // Allocator state (device).  Pops during one footprint kernel only read the

@@ -470,22 +470,23 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   {
     ProfScope ps(v, 2);
     if (memo) {
-      const long long npix = static_cast<long long>(kf->width) * kf->height;
-      k_kf_hash<<<v->n_sms * 4, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
-                                                      &v->d_ops[op].kf_hash);
       fp.kf_hash = &v->d_ops[op].kf_hash;
       fp.use_full = &v->d_ops[op].use_full;
       fp.memo = memo;
-      launches += 1;
-      if (existed) {
-        k_footprint_cached<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
+      if (existed) {  // the guard must be known before the cached keys are used
+        const long long npix = static_cast<long long>(kf->width) * kf->height;
+        k_kf_hash<<<v->n_sms * 4, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
+                                                        &v->d_ops[op].kf_hash);
         launches += 1;
+      } else {  // a new entry samples the rays anyway: hash the planes there
+        fp.hash_inline = 1;
       }
     }
+    // cached key list or full ray sampling (decided on the device), then
+    // the allocation of the missing blocks
     k_footprint<false><<<footprint_grid(v, kf), 256, 0, v->stream>>>(v->T, fp);
-    k_resolve_spill<<<v->n_sms, 256, 0, v->stream>>>(v->T, fp);
     k_commit<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
-    launches += 3;
+    launches += 2;
   }
   FuseParams p = fuse_params(v, kf, pose, op);
   p.capture = memo;
