@@ -1,6 +1,7 @@
-"""Aggregate an ncu --set full report's SASS source page for one kernel:
-stall samples and executed warp-instructions per opcode class, plus the
-hottest instructions.  Usage: ncu_sass_profile.py REPORT KERNEL_SUBSTR [N]"""
+"""Aggregate an ncu --set full report's SASS source page for one kernel
+launch: stall samples and executed warp-instructions per opcode class, plus
+the hottest instructions.
+Usage: ncu_sass_profile.py REPORT KERNEL_SUBSTR [TOP] [NTH_LAUNCH]"""
 import collections
 import csv
 import io
@@ -9,6 +10,7 @@ import sys
 
 rep, ksub = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+nth = int(sys.argv[4]) if len(sys.argv) > 4 else 0  # which launch of the matching kernel
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 blocks, cur = [], None
@@ -18,9 +20,8 @@ for line in out.splitlines():
         blocks.append(cur)
     elif cur is not None:
         cur[1].append(line)
-for name, lines in blocks:
-    if ksub not in name:
-        continue
+matches = [(n, l) for n, l in blocks if ksub in n]
+for name, lines in matches[nth:nth + 1]:
     rows = list(csv.reader(io.StringIO("\n".join(lines))))
     h = rows[0]
     si, ii, src = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed"), h.index("Source")
