@@ -430,3 +430,20 @@ def test_merged_pairs_extreme_values(V, merged_pairs):
     assert V.correct_entries(store, ents, cfg) == 1
     ref.correct_entries(rents)
     assert_same_state(store, ref)
+
+
+@pytest.mark.parametrize("vs", [0.01, 0.005, 0.004])
+def test_footprint_far_from_origin_matches_oracle(V, vs):
+    """The footprint kernel skips samples whose affine block estimate is
+    provably inside the previous sample's block; far from the origin the
+    block coordinates are large (~1e5 spans) and the estimate's rounding
+    largest -- the key set must still be the oracle's, bit for bit."""
+    rng = np.random.default_rng(int(vs * 1e4))
+    cfg = V.VolumeConfig(voxel_size=vs, mu=0.06, stream_radius=1e7)
+    for t in ([0.0, 0.0, 0.0], [3000.0, -1200.0, 41.0], [-2.5e3, 7.0e2, -9.0e2]):
+        f = _vga_frame(rng, z=1.3, tilt=0.2)
+        pose = S.SPose(S.rot_z(rng.uniform(-3, 3)) @ S.rot_y(rng.uniform(-1, 1)), t)
+        got = V.pack_keys(V.keyframe_block_footprint(f, pose, cfg)).tolist()
+        want = O.footprint_keys(f.depth, f.weight, f.intrinsics, pose.rotation,
+                                pose.translation, vs, cfg.mu)
+        assert sorted(got) == sorted(np.asarray(want).tolist())
