@@ -151,6 +151,12 @@ struct KfView {
   double fx, fy, cx, cy;
 };
 
+// Programmatic dependent launch (sm_90+): batch kernels are launched with
+// programmatic stream serialization, so a kernel's CTAs are scheduled while
+// its predecessor drains; each waits here before reading anything the
+// predecessor (or, transitively, earlier work) produced.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ bool ws_skip(const WinState* ws, int op_index) {
   const int kind = *reinterpret_cast<const volatile int*>(&ws->err_kind);
   return kind != kErrNone && *reinterpret_cast<const volatile int*>(&ws->err_op) < op_index;

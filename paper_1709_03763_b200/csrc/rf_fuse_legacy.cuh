@@ -199,6 +199,7 @@ __device__ __forceinline__ void bulk_prefetch_block(const Table& T, const double
 template <int kMode>
 __global__ void __launch_bounds__(kFuseThreads, kMode == kCheckRemove ? 5 : 4)
     k_fuse_legacy(Table T, FuseParams p) {
+  griddep_wait();
   // the first kernel after a footprint kernel folds the allocator state
   if ((kMode == kIntegrate || kMode == kCheckRemove) && blockIdx.x == 0) alloc_fixup_cta(T);
   if (ws_skip(p.ws, p.op_index)) return;

@@ -171,6 +171,27 @@ double sqrt_le_bound(double r) {
   return x;
 }
 
+// Launch a batch kernel with programmatic stream serialization (PDL): its
+// CTAs may be scheduled while the previous kernel drains; every batch kernel
+// starts with griddep_wait().  RF_PDL=0 turns it off (A/B).
+bool g_pdl = true;
+
+template <typename... KArgs, typename... Args>
+void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+            Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 KfView to_view(const rf_kf_view* kf) {
   KfView k;
   k.depth = kf->depth;
@@ -240,7 +261,7 @@ rf_status batch_begin(rf_volume* v, Batch& b, int max_ops) {
   b.has_center = v->has_center;
   std::memcpy(b.center, v->center, sizeof(b.center));
   const int n = std::max(max_ops, 1);
-  k_reset_ops<<<(n + 127) / 128, 128, 0, v->stream>>>(v->d_ops, n, v->d_ws);
+  launch(k_reset_ops, (n + 127) / 128, 128, 0, v->stream, v->d_ops, n, v->d_ws);
   if (v->profiling) v->prof_launches += 1;
   return RF_OK;
 }
@@ -270,7 +291,7 @@ void op_stream(Batch& b, const double c[3]) {
   // tiers are a function of the centre: an unchanged centre moves nothing
   const bool same = b.has_center && c[0] == b.center[0] && c[1] == b.center[1] && c[2] == b.center[2];
   if (!same) {
-    k_stream<<<v->n_sms * 4, 256, 0, v->stream>>>(v->T, p);
+    launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, p);
     if (v->profiling) v->prof_launches += 1;
   }
   // relocation (volume.py:358-364): centre moved more than one block span
@@ -427,8 +448,8 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
   FpEntry* dev = reinterpret_cast<FpEntry*>(mem);
   // initialise the descriptor on the stream (a pageable host->device copy
   // would synchronise the host with the stream mid-batch)
-  k_memo_init<<<1, 1, 0, v->stream>>>(dev, reinterpret_cast<long long*>(mem + head),
-                                      v->memo_slot_cap);
+  launch(k_memo_init, 1, 1, 0, v->stream, dev, reinterpret_cast<long long*>(mem + head),
+         v->memo_slot_cap);
   v->memo_lru.push_front(key);
   MemoSlot ms;
   ms.dev = dev;
@@ -442,9 +463,9 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
 template <int kMode>
 void launch_fuse(rf_volume* v, const FuseParams& p) {
   if (v->legacy_fuse)
-    k_fuse_legacy<kMode><<<v->legacy_grids[kMode], kFuseThreads, 0, v->stream>>>(v->T, p);
+    launch(k_fuse_legacy<kMode>, v->legacy_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
   else
-    k_fuse<kMode><<<v->fuse_grids[kMode], kFuseThreads, 0, v->stream>>>(v->T, p);
+    launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
 }
 
 // mode: 0 integrate, 1 deintegrate, 2 allocate only.  defer_removal (mode
@@ -475,8 +496,8 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
       fp.memo = memo;
       if (existed) {  // the guard must be known before the cached keys are used
         const long long npix = static_cast<long long>(kf->width) * kf->height;
-        k_kf_hash<<<v->n_sms * 4, 256, 0, v->stream>>>(kf->depth, kf->weight, npix,
-                                                        &v->d_ops[op].kf_hash);
+        launch(k_kf_hash, v->n_sms * 4, 256, 0, v->stream, kf->depth, kf->weight, npix,
+               &v->d_ops[op].kf_hash);
         launches += 1;
       } else {  // a new entry samples the rays anyway: hash the planes there
         fp.hash_inline = 1;
@@ -484,8 +505,8 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     }
     // cached key list or full ray sampling (decided on the device), then
     // the allocation of the missing blocks
-    k_footprint<false><<<footprint_grid(v, kf), 256, 0, v->stream>>>(v->T, fp);
-    k_commit<<<v->n_sms * 2, 256, 0, v->stream>>>(v->T, fp);
+    launch(k_footprint<false>, footprint_grid(v, kf), 256, 0, v->stream, v->T, fp);
+    launch(k_commit, v->n_sms * 2, 256, 0, v->stream, v->T, fp);
     launches += 2;
   }
   FuseParams p = fuse_params(v, kf, pose, op);
@@ -502,8 +523,8 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   if (mode == 0 && merge) {
     {
       ProfScope ps(v, 0);
-      k_fuse_merged<<<v->merged_grid, kFuseThreads, kMergedSmemBytes, v->stream>>>(
-          v->T, b.pending_p, p);
+      launch(k_fuse_merged, v->merged_grid, kFuseThreads, kMergedSmemBytes, v->stream, v->T,
+             b.pending_p, p);
     }
     b.infos[b.pending_rm].merged = true;
     b.infos[op].merged = true;
@@ -555,8 +576,8 @@ void op_gc(Batch& b) {
     v->gc_epoch = 1;
   }
   // freed count lands in the op's n_new field
-  k_gc<<<v->n_sms * 8, 256, 0, v->stream>>>(v->T, op, v->d_ws, &v->d_ops[op].n_new,
-                                             v->d_gc_stamp, v->gc_epoch);
+  launch(k_gc, v->n_sms * 8, 256, 0, v->stream, v->T, op, v->d_ws, &v->d_ops[op].n_new,
+         v->d_gc_stamp, v->gc_epoch);
   if (v->profiling) v->prof_launches += 1;
 }
 
@@ -708,6 +729,8 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   {
     const char* impl = std::getenv("RF_FUSE_IMPL");
     v->legacy_fuse = impl && std::string(impl) == "legacy";
+    const char* pdl = std::getenv("RF_PDL");
+    g_pdl = !(pdl && std::string(pdl) == "0");
     const char* mp = std::getenv("RF_MERGE_PAIRS");
     v->merge_pairs = mp && std::string(mp) == "1";
   }
