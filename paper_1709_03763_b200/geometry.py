@@ -54,7 +54,11 @@ class Pose:
         return cls(np.eye(3), np.zeros(3))
 
     def copy(self):
-        return Pose(self.rotation.copy(), self.translation.copy())
+        # a copy of a validated pose is valid: skip __post_init__'s checks
+        out = object.__new__(Pose)
+        out.rotation = self.rotation.copy()
+        out.translation = self.translation.copy()
+        return out
 
 
 def transform(T, p):

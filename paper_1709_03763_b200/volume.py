@@ -145,14 +145,11 @@ def _check(vol_ptr, status, what):
 
 
 def pose_struct(pose):
-    p = L.RfPose()
-    R = np.ascontiguousarray(np.asarray(pose.rotation, dtype=np.float64)).reshape(9)
-    t = np.ascontiguousarray(np.asarray(pose.translation, dtype=np.float64)).reshape(3)
-    for i in range(9):
-        p.R[i] = float(R[i])
-    for i in range(3):
-        p.t[i] = float(t[i])
-    return p
+    """rf_pose (R row-major, t) from a pose; one buffer copy."""
+    buf = np.empty(12, dtype=np.float64)
+    buf[:9] = np.asarray(pose.rotation, dtype=np.float64).reshape(9)
+    buf[9:] = np.asarray(pose.translation, dtype=np.float64).reshape(3)
+    return L.RfPose.from_buffer_copy(buf)
 
 
 def _is_device(arr, device):
