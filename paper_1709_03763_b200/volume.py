@@ -154,7 +154,18 @@ def pose_struct(pose):
 
 def _is_device(arr, device):
     torch = _torch()
-    return isinstance(arr, torch.Tensor) and arr.is_cuda and arr.device.index == device
+    return isinstance(arr, torch.Tensor) and arr.is_cuda and arr.get_device() == device
+
+
+def _ready_plane(arr, shape, device):
+    """The plane itself when it can be passed by pointer as is (CUDA float64
+    contiguous tensor of the right shape on `device`), else None."""
+    torch = _torch()
+    if (isinstance(arr, torch.Tensor) and arr.is_cuda and arr.dtype == torch.float64
+            and arr.get_device() == device and arr.is_contiguous()
+            and tuple(arr.shape) == shape):
+        return arr
+    return None
 
 
 def _device_plane(arr, shape, device):
@@ -190,9 +201,12 @@ def kf_view(kf, device=0, copy_stream=None):
     planes = [(kf.depth, (h, w)), (kf.weight, (h, w))]
     if color is not None:
         planes.append((color, (h, w, 3)))
+    ready = [_ready_plane(a, shp, device) for a, shp in planes]
     on_host = any(not _is_device(a, device) for a, _ in planes)
     event = None
-    if on_host and copy_stream is not None:
+    if all(t is not None for t in ready):  # resident planes: pointers only
+        ts = ready
+    elif on_host and copy_stream is not None:
         consumer = torch.cuda.current_stream(device)
         with torch.cuda.stream(copy_stream):
             ts = [_device_plane(a, shp, device) for a, shp in planes]
@@ -271,9 +285,13 @@ class TwoTierStore:
     def _call(self, name, *args):
         torch = _torch()
         lib = L.lib()
-        with torch.cuda.device(self.device):
+        if torch.cuda.current_device() == self.device:  # the common case: no context switch
             lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
             st = getattr(lib, name)(self._ptr, *args)
+        else:
+            with torch.cuda.device(self.device):
+                lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
+                st = getattr(lib, name)(self._ptr, *args)
         _check(self._ptr, st, name)
 
     def _copy_stream(self):
