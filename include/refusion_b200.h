@@ -73,6 +73,12 @@ typedef struct rf_kf_view {
      * reads this keyframe, so host->device uploads overlap earlier entries'
      * fusion inside one batched call. */
     void *ready_event;
+    /* Identity of the keyframe's planes for the footprint memo, or 0 (the
+     * device pointers are the identity).  Callers uploading host planes per
+     * call pass a stable tag (e.g. the host buffer's address) so that a
+     * de-integration can reuse the footprint of the matching integration;
+     * the memo still validates the planes by content hash. */
+    uint64_t memo_tag;
 } rf_kf_view;
 
 /* IntegrationRecord counts (src/refusion/volume.py:126-134). */

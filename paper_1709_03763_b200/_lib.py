@@ -54,6 +54,7 @@ class RfKfView(ctypes.Structure):
         ("cx", ctypes.c_double),
         ("cy", ctypes.c_double),
         ("ready_event", ctypes.c_void_p),
+        ("memo_tag", ctypes.c_uint64),
     ]
 
 

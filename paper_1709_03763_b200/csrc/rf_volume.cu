@@ -370,8 +370,13 @@ int footprint_grid(rf_volume* v, const rf_kf_view* kf) {
 MemoKey memo_key(const rf_kf_view* kf, const rf_pose* pose) {
   MemoKey k;
   std::memset(&k, 0, sizeof(k));
-  k.depth = kf->depth;
-  k.weight = kf->weight;
+  if (kf->memo_tag) {  // caller-supplied identity (planes uploaded per call)
+    k.depth = reinterpret_cast<const void*>(static_cast<uintptr_t>(kf->memo_tag));
+    k.weight = nullptr;
+  } else {
+    k.depth = kf->depth;
+    k.weight = kf->weight;
+  }
   k.width = kf->width;
   k.height = kf->height;
   k.intr[0] = kf->fx;

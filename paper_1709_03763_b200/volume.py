@@ -225,6 +225,10 @@ def kf_view(kf, device=0, copy_stream=None):
     v.width, v.height = w, h
     v.fx, v.fy, v.cx, v.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
     v.ready_event = event.cuda_event if event is not None else None
+    if on_host and isinstance(kf.depth, torch.Tensor) and isinstance(kf.weight, torch.Tensor):
+        # uploaded per call: the host planes' addresses identify the keyframe
+        # for the footprint memo (content-hash validated on the device)
+        v.memo_tag = (kf.depth.data_ptr() * 0x9E3779B1 ^ kf.weight.data_ptr()) & ((1 << 64) - 1) or 1
     return v, (depth, weight, color_t, event)
 
 
