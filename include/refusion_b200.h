@@ -79,6 +79,11 @@ typedef struct rf_kf_view {
      * de-integration can reuse the footprint of the matching integration;
      * the memo still validates the planes by content hash. */
     uint64_t memo_tag;
+    /* 1: depth / weight / color are HOST pointers (pinned for asynchronous
+     * copies): the volume stages them on its copy stream into device slots,
+     * each entry's kernels waiting only for its own upload, so uploads
+     * overlap the fusion of earlier entries.  0: device pointers. */
+    int32_t planes_on_host;
 } rf_kf_view;
 
 /* IntegrationRecord counts (src/refusion/volume.py:126-134). */

@@ -55,6 +55,7 @@ class RfKfView(ctypes.Structure):
         ("cy", ctypes.c_double),
         ("ready_event", ctypes.c_void_p),
         ("memo_tag", ctypes.c_uint64),
+        ("planes_on_host", ctypes.c_int32),
     ]
 
 

@@ -98,6 +98,17 @@ struct rf_volume {
   bool legacy_fuse = false;  // RF_FUSE_IMPL=legacy: whole-block-prefetch A/B baseline
   int merged_grid = 148;
   bool merge_pairs = false;  // RF_MERGE_PAIRS=1 enables k_fuse_merged
+  // staging of host keyframe planes (rf_kf_view.planes_on_host)
+  struct StageSlot {
+    double* buf = nullptr;
+    size_t cap = 0;  // doubles
+    cudaEvent_t ready = nullptr, consumed = nullptr;
+    const void* host = nullptr;  // host depth pointer staged in this batch
+    bool used = false;
+  };
+  std::vector<StageSlot> stage;
+  cudaStream_t copy_stream = nullptr;
+  int stage_next = 0;
   int fp_grid_cap = 148 * 8;
   // footprint memo
   std::unordered_map<MemoKey, MemoSlot, MemoKeyHash> memo;
@@ -473,6 +484,88 @@ void launch_fuse(rf_volume* v, const FuseParams& p) {
     launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
 }
 
+// Host keyframe planes (planes_on_host): copy each distinct keyframe of a
+// call (one correction window, or one op) once, on the volume's copy stream,
+// into a ring of device slots; the returned views carry device pointers and
+// the slot's ready event (the compute stream waits on it just before that
+// entry's first kernel).  A slot is refilled only after the compute stream
+// passed its previous occupant's last consumer (stage_consumed, recorded by
+// an earlier window).  Returns the slot per view (-1: device view).
+constexpr int kStageSlots = 16;
+
+rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_kf_view>& out,
+                      std::vector<int>& slot_of) {
+  out.assign(in, in + n);
+  slot_of.assign(n, -1);
+  bool any = false;
+  for (int i = 0; i < n; ++i) any |= in[i].planes_on_host != 0;
+  if (!any) return RF_OK;
+  if (!v->copy_stream)
+    RF_CUDA_TRY(v, cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking));
+  // every entry of one call (window) must be resident at once
+  const size_t ring = std::max<size_t>(kStageSlots, static_cast<size_t>(n));
+  if (v->stage.size() < ring) v->stage.resize(ring);
+  for (auto& sl : v->stage) sl.host = nullptr;
+  for (int i = 0; i < n; ++i) {
+    const rf_kf_view& k = in[i];
+    if (!k.planes_on_host) continue;
+    int reuse = -1;  // the same keyframe earlier in this batch
+    for (int j = 0; j < i; ++j)
+      if (slot_of[j] >= 0 && in[j].depth == k.depth && in[j].weight == k.weight &&
+          in[j].color == k.color) {
+        reuse = slot_of[j];
+        break;
+      }
+    const size_t npix = static_cast<size_t>(k.width) * k.height;
+    if (reuse < 0 || v->stage[reuse].host != k.depth) {
+      const int s = v->stage_next;
+      v->stage_next = (v->stage_next + 1) % static_cast<int>(v->stage.size());
+      auto& sl = v->stage[s];
+      const size_t need = npix * (k.color ? 5 : 2);
+      if (sl.cap < need) {
+        RF_CUDA_TRY(v, cudaStreamSynchronize(v->copy_stream));
+        RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+        if (sl.buf) cudaFree(sl.buf);
+        sl.buf = nullptr;
+        RF_CUDA_TRY(v, cudaMalloc(&sl.buf, sizeof(double) * need));
+        sl.cap = need;
+      }
+      if (!sl.ready) RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+      if (!sl.consumed)
+        RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+      if (sl.used) cudaStreamWaitEvent(v->copy_stream, sl.consumed, 0);
+      cudaMemcpyAsync(sl.buf, k.depth, sizeof(double) * npix, cudaMemcpyHostToDevice, v->copy_stream);
+      cudaMemcpyAsync(sl.buf + npix, k.weight, sizeof(double) * npix, cudaMemcpyHostToDevice,
+                      v->copy_stream);
+      if (k.color)
+        cudaMemcpyAsync(sl.buf + 2 * npix, k.color, sizeof(double) * 3 * npix,
+                        cudaMemcpyHostToDevice, v->copy_stream);
+      RF_CUDA_TRY(v, cudaEventRecord(sl.ready, v->copy_stream));
+      sl.used = true;
+      sl.host = k.depth;
+      reuse = s;
+    }
+    const auto& sl = v->stage[reuse];
+    slot_of[i] = reuse;
+    rf_kf_view& o = out[i];
+    o.depth = sl.buf;
+    o.weight = sl.buf + npix;
+    o.color = k.color ? sl.buf + 2 * npix : nullptr;
+    o.ready_event = sl.ready;
+    o.planes_on_host = 0;
+    // the host planes identify the keyframe for the footprint memo
+    if (!o.memo_tag) o.memo_tag = reinterpret_cast<uintptr_t>(k.depth) * 0x9E3779B97F4A7C15ull ^
+                                  reinterpret_cast<uintptr_t>(k.weight);
+  }
+  return RF_OK;
+}
+
+// The compute stream passed every use of view i's staged planes.
+void stage_consumed(rf_volume* v, const std::vector<int>& slot_of, int i) {
+  if (i < static_cast<int>(slot_of.size()) && slot_of[i] >= 0)
+    cudaEventRecord(v->stage[slot_of[i]].consumed, v->stream);
+}
+
 // mode: 0 integrate, 1 deintegrate, 2 allocate only.  defer_removal (mode
 // 1): run the removal check now but leave the removal to the next op, which
 // must be an integration called with merge = true: the two become one
@@ -813,6 +906,12 @@ rf_status rf_volume_destroy(rf_volume* v) {
   }
   for (auto e : v->event_pool) cudaEventDestroy(e);
   memo_release(v);
+  for (auto& sl : v->stage) {
+    if (sl.buf) cudaFree(sl.buf);
+    if (sl.ready) cudaEventDestroy(sl.ready);
+    if (sl.consumed) cudaEventDestroy(sl.consumed);
+  }
+  if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
   delete v;
   return RF_OK;
 }
@@ -845,6 +944,13 @@ rf_status rf_footprint(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
                        int64_t cap, int64_t* n_out) {
   if (!v || !valid_kf(kf) || !pose || !n_out) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
+  std::vector<rf_kf_view> staged;
+  std::vector<int> slot_of;
+  {
+    const rf_status sst = stage_views(v, kf, 1, staged, slot_of);
+    if (sst != RF_OK) return sst;
+    kf = staged.data();
+  }
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -889,6 +995,13 @@ rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
                       int64_t* new_keys_host, int64_t cap, int64_t* n_new) {
   if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
+  std::vector<rf_kf_view> staged;
+  std::vector<int> slot_of;
+  {
+    const rf_status sst = stage_views(v, kf, 1, staged, slot_of);
+    if (sst != RF_OK) return sst;
+    kf = staged.data();
+  }
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -905,6 +1018,13 @@ rf_status rf_integrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
                        rf_op_result* result, int64_t* new_keys_host, int64_t new_cap) {
   if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
+  std::vector<rf_kf_view> staged;
+  std::vector<int> slot_of;
+  {
+    const rf_status sst = stage_views(v, kf, 1, staged, slot_of);
+    if (sst != RF_OK) return sst;
+    kf = staged.data();
+  }
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -925,6 +1045,13 @@ rf_status rf_deintegrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose
                          rf_op_result* result) {
   if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
+  std::vector<rf_kf_view> staged;
+  std::vector<int> slot_of;
+  {
+    const rf_status sst = stage_views(v, kf, 1, staged, slot_of);
+    if (sst != RF_OK) return sst;
+    kf = staged.data();
+  }
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -968,7 +1095,14 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
   for (int w = 0; w < n_windows; ++w) {
     const int m = sizes[w];
     if (m == 0) continue;  // :161-162
-    const rf_kf_view* k = kfs + base;
+    // host planes: staged per window (uploads overlap earlier windows' work)
+    std::vector<rf_kf_view> staged;
+    std::vector<int> slot_of;
+    {
+      const rf_status sst = stage_views(v, kfs + base, m, staged, slot_of);
+      if (sst != RF_OK) return sst;
+    }
+    const rf_kf_view* k = staged.data();
     const rf_pose* o = old_poses + base;
     const rf_pose* n = new_poses + base;
     op_stream(b, o[0].t);
@@ -983,6 +1117,7 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
       op_stream(b, n[i].t);
       op_fuse(b, &k[i], &n[i], 0, i, false, /*merge=*/i == 0);
       b.infos.back().window = w;
+      stage_consumed(v, slot_of, i);  // last use of its planes
     }
     op_gc(b);
     b.infos.back().window = w;
@@ -1023,12 +1158,16 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
   if (out.err_kind == kErrInconsistent && bad.kind == 2 && bad.entry > 0) {
     // reintegration.py:170-174: re-integrate what was already removed
     const std::string msg = v->err;
+    std::vector<rf_kf_view> staged;
+    std::vector<int> slot_of;
+    st = stage_views(v, kfs + wbase, bad.entry, staged, slot_of);
+    if (st != RF_OK) return st;
     Batch rb;
     st = batch_begin(v, rb, 2 * bad.entry);
     if (st != RF_OK) return st;
     for (int i = 0; i < bad.entry; ++i) {
       op_stream(rb, old_poses[wbase + i].t);
-      op_fuse(rb, &kfs[wbase + i], &old_poses[wbase + i], 0, i);
+      op_fuse(rb, &staged[i], &old_poses[wbase + i], 0, i);
     }
     BatchOutcome ro;
     st = batch_end(rb, ro);

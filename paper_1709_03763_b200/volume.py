@@ -152,11 +152,6 @@ def pose_struct(pose):
     return L.RfPose.from_buffer_copy(buf)
 
 
-def _is_device(arr, device):
-    torch = _torch()
-    return isinstance(arr, torch.Tensor) and arr.is_cuda and arr.get_device() == device
-
-
 def _ready_plane(arr, shape, device):
     """The plane itself when it can be passed by pointer as is (CUDA float64
     contiguous tensor of the right shape on `device`), else None."""
@@ -186,14 +181,31 @@ def _device_plane(arr, shape, device):
     return t
 
 
-def kf_view(kf, device=0, copy_stream=None):
+def _host_plane(arr, shape):
+    """(host address, keep-alive) of a plane held in host memory: a CPU torch
+    tensor (pinned for asynchronous copies) or anything numpy accepts."""
+    torch = _torch()
+    if isinstance(arr, torch.Tensor):
+        t = arr.detach()
+        if t.dtype != torch.float64 or not t.is_contiguous():
+            t = t.to(torch.float64).contiguous()
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"keyframe plane shape {tuple(t.shape)} != {tuple(shape)}")
+        return t.data_ptr(), t
+    a = np.ascontiguousarray(np.asarray(arr, dtype=np.float64))
+    if a.shape != tuple(shape):
+        raise ValueError(f"keyframe plane shape {a.shape} != {tuple(shape)}")
+    return a.ctypes.data, a
+
+
+def kf_view(kf, device=0):
     """(rf_kf_view, keep-alive objects) for a duck-typed keyframe.
 
-    Planes already on the device are passed by pointer.  Host planes are
-    uploaded; with ``copy_stream`` the upload is issued there (pinned host
-    memory makes it asynchronous) and the view carries a ready event the
-    volume's stream waits on, so uploads overlap the fusion of earlier
-    entries of a batched call."""
+    CUDA float64 planes on `device` are passed by pointer.  Planes in host
+    memory (numpy, CPU / pinned torch tensors) are passed as host pointers:
+    the library stages them on its copy stream, so a batched call's uploads
+    overlap the fusion of its earlier entries.  Planes on another GPU are
+    copied here."""
     torch = _torch()
     intr = kf.intrinsics
     h, w = int(intr.height), int(intr.width)
@@ -201,35 +213,22 @@ def kf_view(kf, device=0, copy_stream=None):
     planes = [(kf.depth, (h, w)), (kf.weight, (h, w))]
     if color is not None:
         planes.append((color, (h, w, 3)))
-    ready = [_ready_plane(a, shp, device) for a, shp in planes]
-    on_host = any(not _is_device(a, device) for a, _ in planes)
-    event = None
-    if all(t is not None for t in ready):  # resident planes: pointers only
-        ts = ready
-    elif on_host and copy_stream is not None:
-        consumer = torch.cuda.current_stream(device)
-        with torch.cuda.stream(copy_stream):
-            ts = [_device_plane(a, shp, device) for a, shp in planes]
-            event = torch.cuda.Event()
-            event.record(copy_stream)
-        for t in ts:
-            t.record_stream(consumer)
-    else:
-        ts = [_device_plane(a, shp, device) for a, shp in planes]
-    depth, weight = ts[0], ts[1]
-    color_t = ts[2] if color is not None else None
     v = L.RfKfView()
-    v.depth = depth.data_ptr()
-    v.weight = weight.data_ptr()
-    v.color = color_t.data_ptr() if color_t is not None else None
     v.width, v.height = w, h
     v.fx, v.fy, v.cx, v.cy = float(intr.fx), float(intr.fy), float(intr.cx), float(intr.cy)
-    v.ready_event = event.cuda_event if event is not None else None
-    if on_host and isinstance(kf.depth, torch.Tensor) and isinstance(kf.weight, torch.Tensor):
-        # uploaded per call: the host planes' addresses identify the keyframe
-        # for the footprint memo (content-hash validated on the device)
-        v.memo_tag = (kf.depth.data_ptr() * 0x9E3779B1 ^ kf.weight.data_ptr()) & ((1 << 64) - 1) or 1
-    return v, (depth, weight, color_t, event)
+    ready = [_ready_plane(a, shp, device) for a, shp in planes]
+    if all(t is not None for t in ready):  # resident planes: pointers only
+        ptrs, keep = [t.data_ptr() for t in ready], ready
+    elif not any(isinstance(a, torch.Tensor) and a.is_cuda for a, _ in planes):
+        pk = [_host_plane(a, shp) for a, shp in planes]
+        ptrs, keep = [p for p, _ in pk], [k for _, k in pk]
+        v.planes_on_host = 1
+    else:  # mixed, or planes on another device: make them resident here
+        keep = [_device_plane(a, shp, device) for a, shp in planes]
+        ptrs = [t.data_ptr() for t in keep]
+    v.depth, v.weight = ptrs[0], ptrs[1]
+    v.color = ptrs[2] if color is not None else None
+    return v, keep
 
 
 # ---------------------------------------------------------------------------
@@ -297,13 +296,6 @@ class TwoTierStore:
                 lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
                 st = getattr(lib, name)(self._ptr, *args)
         _check(self._ptr, st, name)
-
-    def _copy_stream(self):
-        """Side stream for host->device keyframe uploads (created lazily)."""
-        if getattr(self, "_copy", None) is None:
-            torch = _torch()
-            self._copy = torch.cuda.Stream(device=self.device)
-        return self._copy
 
     def close(self):
         if self._ptr is not None:
@@ -568,9 +560,8 @@ def correct_windows(store, windows, cfg, next_center=None):
     news = (L.RfPose * n)()
     sizes = (ctypes.c_int32 * len(windows))(*[len(w) for w in windows])
     keep = []
-    copy_stream = store._copy_stream()
     for i, e in enumerate(entries):
-        v, k = kf_view(e.kf, store.device, copy_stream)
+        v, k = kf_view(e.kf, store.device)
         views[i] = v
         keep.append(k)
         olds[i] = pose_struct(e.integrated_pose)

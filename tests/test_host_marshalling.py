@@ -1,0 +1,45 @@
+"""Host-side marshalling of the C ABI (no GPU needed): keyframe views built
+from host planes carry host pointers for the library to stage, and poses
+are packed row-major with the translation last."""
+
+import numpy as np
+
+from paper_1709_03763_b200 import volume as V
+from paper_1709_03763_b200.geometry import Pose
+
+import scenarios as S
+
+
+def test_host_planes_are_passed_for_staging():
+    rng = np.random.default_rng(3)
+    f = S.random_frame(rng)
+    view, keep = V.kf_view(f, device=0)
+    assert view.planes_on_host == 1
+    assert view.depth == keep[0].ctypes.data and view.weight == keep[1].ctypes.data
+    assert view.color == keep[2].ctypes.data
+    assert (view.width, view.height) == (f.intrinsics.width, f.intrinsics.height)
+    assert not view.ready_event and view.memo_tag == 0  # the library derives the tag
+
+
+def test_host_planes_are_converted_to_contiguous_f64():
+    rng = np.random.default_rng(4)
+    f = S.random_frame(rng)
+    f.depth = np.asfortranarray(f.depth.astype(np.float32))
+    view, keep = V.kf_view(f, device=0)
+    assert keep[0].dtype == np.float64 and keep[0].flags.c_contiguous
+    assert np.array_equal(keep[0], f.depth.astype(np.float64))
+
+
+def test_pose_struct_layout():
+    rng = np.random.default_rng(5)
+    R = S.rot_z(rng.uniform(-3, 3)) @ S.rot_y(rng.uniform(-1, 1))
+    t = rng.uniform(-5, 5, 3)
+    p = V.pose_struct(Pose(R, t))
+    assert list(p.R) == R.reshape(9).tolist() and list(p.t) == t.tolist()
+
+
+def test_pose_copy_is_independent():
+    p = Pose(S.rot_x(0.3), np.array([1.0, 2.0, 3.0]))
+    q = p.copy()
+    q.translation[0] = 9.0
+    assert p.translation[0] == 1.0 and np.array_equal(q.rotation, p.rotation)
