@@ -237,14 +237,16 @@ __global__ void __launch_bounds__(kFuseThreads, kMode == kCheckRemove ? 5 : 4)
   if ((kMode == kIntegrate || kMode == kCheckRemove) && p.capture && op->use_full) {
     // memoise this op's footprint keys for the matching later op
     const int cap = p.capture->cap;
-    if (n <= cap) {
+    const bool sharded = p.shard_count > 1;
+    const int cnt = sharded ? static_cast<int>(op->capture_n) : n;
+    if (!sharded && n <= cap) {
       for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         p.capture->keys[i] = T.keys[static_cast<unsigned>(T.touched[i]) & kSlotMask];
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-      p.capture->count = n;
+      p.capture->count = cnt;
       p.capture->hash = op->kf_hash;
-      p.capture->valid = n <= cap ? 1 : 0;
+      p.capture->valid = cnt <= cap ? 1 : 0;
     }
   }
   if (kMode == kIntegrate && p.alloc_only) {

@@ -369,6 +369,7 @@ FuseParams fuse_params(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
   p.op_index = op;
   p.op = v->d_ops + op;
   p.ws = v->d_ws;
+  p.shard_count = v->cfg.shard_count;
   return p;
 }
 
@@ -425,9 +426,10 @@ void memo_release(rf_volume* v) {
 // Returns the memo entry for (kf, pose) and whether it pre-existed.
 FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bool& existed) {
   existed = false;
-  // a shard's memo would hold only its own keys, but the contract check
-  // must see the whole footprint: sharded volumes sample every time
-  if (v->memo_budget == 0 || v->cfg.shard_count > 1) return nullptr;
+  // (a sharded volume's entries hold the WHOLE footprint -- the contract is
+  // checked on every key -- recorded by its sampling pass, duplicates
+  // across pixel tiles included: room for one key per pixel)
+  if (v->memo_budget == 0) return nullptr;
   const MemoKey key = memo_key(kf, pose);
   auto it = v->memo.find(key);
   if (it != v->memo.end()) {
@@ -436,7 +438,9 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
     return it->second.dev;
   }
   const long long npix = static_cast<long long>(kf->width) * kf->height;
-  const int cap = static_cast<int>(std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
+  const int cap = static_cast<int>(
+      v->cfg.shard_count > 1 ? std::max(4096LL, npix)
+                             : std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
   const size_t head = (sizeof(FpEntry) + 15) & ~size_t(15);
   if (!v->memo_arena) {  // first use: slots sized for this keyframe
     const size_t slot = (head + sizeof(long long) * static_cast<size_t>(cap) + 255) & ~size_t(255);
@@ -578,7 +582,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
-  merge = merge && mode == 0 && b.pending_rm >= 0;
+  merge = merge && mode == 0 && b.pending_rm >= 0 && v->cfg.shard_count == 1;
   if (merge) {
     fp.merge_op = v->d_ops + b.pending_rm;
     fp.merge_epoch = b.pending_epoch;
@@ -639,7 +643,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     }
     p.capture = nullptr;
     launches += 1;
-    if (defer_removal && v->merge_pairs && !v->legacy_fuse) {
+    if (defer_removal && v->merge_pairs && !v->legacy_fuse && v->cfg.shard_count == 1) {
       b.pending_rm = op;
       b.pending_p = p;
       b.pending_epoch = fp.epoch;
