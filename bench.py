@@ -206,6 +206,12 @@ def run_b200(args):
     cfg = V.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS, hash_buckets=1 << 21)
     cap = int(os.environ.get("RF_BENCH_BLOCKS", str(2_600_000 // world + 200_000)))
     store = V.TwoTierStore(block_capacity=cap, shard_rank=rank, shard_count=world)
+    # RF_ROUTE=1: footprints sampled 1/G per shard, keys stored into the owners'
+    # inboxes (rf_route).  Off by default: on this workload the replicated
+    # sampling with its footprint memo costs less per shard.
+    routed = world > 1 and os.environ.get("RF_ROUTE", "0") == "1"
+    if routed:
+        V.connect_shards_distributed(store, cfg)
     n_events = args.warmup + 2 * args.steps + 2
     scen = Scenario(R, G, SY, gt_kf, drifted, keyframes,
                     make_events((n_kf + EVENT_EVERY_KF - 1) // EVENT_EVERY_KF, n_events))
@@ -371,7 +377,8 @@ def run_b200(args):
                    "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS,
                    "hash_buckets": cfg.hash_buckets, "blocks_resident": n_blocks,
                    "block_capacity": cap, "volume_build_s": round(build_s, 2),
-                   "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+                   "parallelism": (f"hash-sharded x{world}" + (", routed footprints" if routed else ""))
+                   if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MiB write, outside the step events)"},
         "gpu_launches": int(round(prof.kernel_launches * args.steps / prof_steps)),
         "step_ms": [round(t, 3) for t in times],

@@ -137,6 +137,8 @@ typedef struct rf_profile {
     int64_t pixels;              /* keyframe pixels read by profiled fuse launches */
     int64_t blocks_touched;
     int64_t kernel_launches;     /* every kernel this library launched while profiling */
+    int64_t other_launches;      /* streaming, GC and bookkeeping kernels */
+    double other_ms;
 } rf_profile;
 
 /* ---- lifecycle ------------------------------------------------------- */
@@ -221,6 +223,32 @@ rf_status rf_fuse_block(double *d, double *w, double *c,
  * produced, so the matching de-integration skips the ray sampling; a 64-bit
  * content hash of the depth/weight planes guards against in-place edits. */
 rf_status rf_set_memo_budget(rf_volume *vol, int64_t bytes);
+
+/* ---- routed footprints (hash-sharded volumes) ---------------
+ * No reference counterpart: the reference is one process (volume.py:151-249
+ * is what these split across shards).  Once connected, every footprint op
+ * of a shard is sampled cooperatively: rf_route makes shard r sample the
+ * pixel tiles t with t mod shard_count == r and store each distinct block
+ * key straight into its owner's inbox (peer memory over NVLink), then
+ * synchronises.  After a barrier across the shards (the caller's:
+ * torch.distributed, threads ...) the next rf_allocate / rf_integrate /
+ * rf_deintegrate (1 op) or rf_correct_windows (per window: its m removal
+ * footprints, then its m integration footprints) consumes those inboxes --
+ * exactly that many ops, else RF_INVALID_ARG.  centers (3 per op, may be
+ * NULL = the volume's current centre) is the streaming centre each op's
+ * contract is checked against.  The footprint memo is off when routed. */
+/* allocate this shard's inbox: max_ops footprints per call, cap_keys keys
+ * per (op, sending shard); *inbox / *bytes describe the device buffer */
+rf_status rf_route_setup(rf_volume *vol, int32_t max_ops, int64_t cap_keys, void **inbox,
+                         uint64_t *bytes);
+/* shards of one process: inboxes[s] = shard s's inbox (device pointers) */
+rf_status rf_route_connect(rf_volume *vol, void *const *inboxes);
+/* shards in separate processes: 64-byte cudaIpcMemHandle_t of this inbox,
+ * and open all shards' handles (shard_count x 64 bytes, own entry ignored) */
+rf_status rf_route_ipc_handle(rf_volume *vol, void *handle);
+rf_status rf_route_ipc_open(rf_volume *vol, const void *handles);
+rf_status rf_route(rf_volume *vol, int32_t n, const rf_kf_view *kfs, const rf_pose *poses,
+                   const double *centers);
 
 /* ---- measurement -------------------------------------------------------- */
 rf_status rf_profile_begin(rf_volume *vol);

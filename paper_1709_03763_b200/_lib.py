@@ -114,6 +114,8 @@ class RfProfile(ctypes.Structure):
         ("pixels", ctypes.c_int64),
         ("blocks_touched", ctypes.c_int64),
         ("kernel_launches", ctypes.c_int64),
+        ("other_launches", ctypes.c_int64),
+        ("other_ms", ctypes.c_double),
     ]
 
 
@@ -206,6 +208,13 @@ SIGNATURES = {
                                     ctypes.c_double, ctypes.c_uint64, ctypes.c_uint64,
                                     ctypes.POINTER(ctypes.c_uint64)]),
     "rf_set_memo_budget": (_S, [_vp, ctypes.c_int64]),
+    "rf_route_setup": (_S, [_vp, ctypes.c_int32, ctypes.c_int64, ctypes.POINTER(_vp),
+                            ctypes.POINTER(ctypes.c_uint64)]),
+    "rf_route_connect": (_S, [_vp, ctypes.POINTER(_vp)]),
+    "rf_route_ipc_handle": (_S, [_vp, _vp]),
+    "rf_route_ipc_open": (_S, [_vp, _vp]),
+    "rf_route": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
+                      c_double_p]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
     "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4

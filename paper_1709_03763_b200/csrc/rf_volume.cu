@@ -126,6 +126,15 @@ struct rf_volume {
   std::vector<EventPair> events;
   std::vector<cudaEvent_t> event_pool;
   long long prof_voxels = 0, prof_pixels = 0, prof_blocks = 0, prof_launches = 0;
+  // routed footprints (hash-sharded volume, k_route): this shard's inbox and
+  // every shard's (peers opened over IPC are closed on destroy)
+  char* route_own = nullptr;
+  char* route_peer[kMaxShards] = {};
+  bool route_ipc[kMaxShards] = {};
+  RouteLayout route_lay{};
+  bool route_on = false;
+  unsigned route_gen = 0;
+  int route_nops = 0;  // ops routed by the last rf_route, consumed by the next call
   std::string err;
 };
 
@@ -251,6 +260,9 @@ struct Batch {
   int pending_rm = -1;
   FuseParams pending_p{};
   unsigned pending_epoch = 0;
+  // routed volume: next inbox op to consume (route_force >= 0 overrides)
+  int route_next = 0;
+  int route_force = -1;
 };
 
 rf_status ensure_ops(rf_volume* v, int n) {
@@ -272,7 +284,10 @@ rf_status batch_begin(rf_volume* v, Batch& b, int max_ops) {
   b.has_center = v->has_center;
   std::memcpy(b.center, v->center, sizeof(b.center));
   const int n = std::max(max_ops, 1);
-  launch(k_reset_ops, (n + 127) / 128, 128, 0, v->stream, v->d_ops, n, v->d_ws);
+  {
+    ProfScope ps(v, 3);
+    launch(k_reset_ops, (n + 127) / 128, 128, 0, v->stream, v->d_ops, n, v->d_ws);
+  }
   if (v->profiling) v->prof_launches += 1;
   return RF_OK;
 }
@@ -302,6 +317,7 @@ void op_stream(Batch& b, const double c[3]) {
   // tiers are a function of the centre: an unchanged centre moves nothing
   const bool same = b.has_center && c[0] == b.center[0] && c[1] == b.center[1] && c[2] == b.center[2];
   if (!same) {
+    ProfScope ps(v, 3);
     launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, p);
     if (v->profiling) v->prof_launches += 1;
   }
@@ -479,6 +495,28 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
   return dev;
 }
 
+
+// A routed volume consumes exactly the footprints its last rf_route sent;
+// the consumed inbox generation is emptied afterwards (on the stream, ahead
+// of the next rf_route, which synchronises before the callers' barrier).
+rf_status route_expect(rf_volume* v, int n) {
+  if (!v->route_on || v->route_nops == n) return RF_OK;
+  return fail(v, RF_INVALID_ARG,
+              "routed volume: rf_route must send exactly this call's footprints first");
+}
+
+struct RouteConsume {
+  rf_volume* v;
+  ~RouteConsume() {
+    if (!v->route_on) return;
+    ProfScope ps(v, 3);
+    launch(k_route_reset, 8, 256, 0, v->stream, v->route_own, v->route_lay,
+           static_cast<int>(v->route_gen & 1));
+    if (v->profiling) v->prof_launches += 1;
+    v->route_nops = 0;
+  }
+};
+
 // Launch the batched fuse kernel of mode kMode (or the legacy A/B baseline).
 template <int kMode>
 void launch_fuse(rf_volume* v, const FuseParams& p) {
@@ -588,7 +626,19 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     fp.merge_epoch = b.pending_epoch;
   }
   bool existed = false;
-  FpEntry* memo = memo_lookup(v, kf, pose, existed);
+  FpEntry* memo = nullptr;
+  if (v->route_on) {  // the footprint arrives in this shard's inbox (k_route)
+    const int idx = b.route_force >= 0 ? b.route_force : b.route_next++;
+    const int par = static_cast<int>(v->route_gen & 1);
+    const RouteLayout& L = v->route_lay;
+    fp.route_keys = reinterpret_cast<const long long*>(v->route_own + L.keys_off(par, idx, 0));
+    fp.route_counts = reinterpret_cast<const unsigned*>(v->route_own + L.count_off(par, idx, 0));
+    fp.route_viol = reinterpret_cast<const long long*>(v->route_own + L.viol_off(par, idx));
+    fp.route_segs = L.shards;
+    fp.route_cap = L.cap;
+  } else {
+    memo = memo_lookup(v, kf, pose, existed);
+  }
   int launches = 0;
   {
     ProfScope ps(v, 2);
@@ -678,6 +728,7 @@ void op_gc(Batch& b) {
     v->gc_epoch = 1;
   }
   // freed count lands in the op's n_new field
+  ProfScope ps(v, 3);
   launch(k_gc, v->n_sms * 8, 256, 0, v->stream, v->T, op, v->d_ws, &v->d_ops[op].n_new,
          v->d_gc_stamp, v->gc_epoch);
   if (v->profiling) v->prof_launches += 1;
@@ -835,6 +886,13 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
     g_pdl = !(pdl && std::string(pdl) == "0");
     const char* mp = std::getenv("RF_MERGE_PAIRS");
     v->merge_pairs = mp && std::string(mp) == "1";
+    const char* gran = std::getenv("RF_L2_FETCH");
+    if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::strtoul(gran, nullptr, 10));
+    if (std::getenv("RF_VERBOSE")) {
+      size_t g = 0;
+      cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
+      std::fprintf(stderr, "rf: L2 fetch granularity %zu B\n", g);
+    }
   }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
@@ -916,6 +974,9 @@ rf_status rf_volume_destroy(rf_volume* v) {
     if (sl.consumed) cudaEventDestroy(sl.consumed);
   }
   if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
+  for (int s = 0; s < kMaxShards; ++s)
+    if (v->route_ipc[s]) cudaIpcCloseMemHandle(v->route_peer[s]);
+  if (v->route_own) cudaFree(v->route_own);
   delete v;
   return RF_OK;
 }
@@ -995,6 +1056,111 @@ rf_status rf_footprint(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, 
   return fail(v, RF_CUDA, "footprint scratch sizing failed");
 }
 
+
+// ---- routed footprints (hash-sharded volumes, k_route) --------------------
+
+rf_status rf_route_setup(rf_volume* v, int32_t max_ops, int64_t cap_keys, void** inbox,
+                         uint64_t* bytes) {
+  if (!v || max_ops <= 0 || cap_keys <= 0 || cap_keys > (1LL << 30) || v->cfg.shard_count < 2 ||
+      v->cfg.shard_count > kMaxShards)
+    return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  if (v->route_own) return fail(v, RF_INVALID_ARG, "rf_route_setup: inbox already set up");
+  RouteLayout L{max_ops, v->cfg.shard_count, static_cast<int>(cap_keys)};
+  void* mem = nullptr;
+  RF_CUDA_TRY(v, cudaMalloc(&mem, L.bytes()));
+  v->route_own = static_cast<char*>(mem);
+  v->route_lay = L;
+  for (int par = 0; par < 2; ++par)
+    k_route_reset<<<8, 256, 0, v->stream>>>(v->route_own, L, par);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  if (inbox) *inbox = mem;
+  if (bytes) *bytes = L.bytes();
+  return RF_OK;
+}
+
+rf_status rf_route_connect(rf_volume* v, void* const* inboxes) {
+  if (!v || !inboxes || !v->route_own) return RF_INVALID_ARG;
+  if (inboxes[v->cfg.shard_rank] != v->route_own)
+    return fail(v, RF_INVALID_ARG, "rf_route_connect: own inbox mismatch");
+  for (int s = 0; s < v->cfg.shard_count; ++s) {
+    if (!inboxes[s]) return RF_INVALID_ARG;
+    v->route_peer[s] = static_cast<char*>(inboxes[s]);
+  }
+  v->route_on = true;
+  return RF_OK;
+}
+
+rf_status rf_route_ipc_handle(rf_volume* v, void* handle) {
+  if (!v || !handle || !v->route_own) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaIpcMemHandle_t h;
+  RF_CUDA_TRY(v, cudaIpcGetMemHandle(&h, v->route_own));
+  std::memcpy(handle, &h, sizeof(h));
+  return RF_OK;
+}
+
+rf_status rf_route_ipc_open(rf_volume* v, const void* handles) {
+  if (!v || !handles || !v->route_own) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  const int G = v->cfg.shard_count;
+  std::vector<void*> ptrs(G, nullptr);
+  for (int s = 0; s < G; ++s) {
+    if (s == v->cfg.shard_rank) {
+      ptrs[s] = v->route_own;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + s * sizeof(h), sizeof(h));
+    RF_CUDA_TRY(v, cudaIpcOpenMemHandle(&ptrs[s], h, cudaIpcMemLazyEnablePeerAccess));
+    v->route_ipc[s] = true;
+  }
+  return rf_route_connect(v, ptrs.data());
+}
+
+rf_status rf_route(rf_volume* v, int32_t n, const rf_kf_view* kfs, const rf_pose* poses,
+                   const double* centers) {
+  if (!v || n < 0 || (n > 0 && (!kfs || !poses))) return RF_INVALID_ARG;
+  if (!v->route_on) return fail(v, RF_INVALID_ARG, "rf_route: inbox not connected");
+  if (n > v->route_lay.max_ops) return fail(v, RF_INVALID_ARG, "rf_route: more ops than the inbox holds");
+  for (int i = 0; i < n; ++i)
+    if (!valid_kf(&kfs[i])) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  std::vector<rf_kf_view> staged;
+  std::vector<int> slot_of;
+  {
+    const rf_status sst = stage_views(v, kfs, n, staged, slot_of);
+    if (sst != RF_OK) return sst;
+  }
+  ++v->route_gen;
+  RouteArgs r{};
+  for (int s = 0; s < v->cfg.shard_count; ++s) r.peer[s] = v->route_peer[s];
+  r.lay = v->route_lay;
+  r.parity = static_cast<int>(v->route_gen & 1);
+  r.rank = v->cfg.shard_rank;
+  for (int i = 0; i < n; ++i) {
+    const rf_kf_view* kf = &staged[i];
+    if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
+    Batch b;  // only the centre is read
+    b.has_center = centers ? true : v->has_center;
+    std::memcpy(b.center, centers ? centers + 3 * i : v->center, sizeof(b.center));
+    FootprintParams fp = footprint_params(v, b, kf, &poses[i], 0);
+    fp.op = nullptr;
+    fp.ws = nullptr;
+    r.op = i;
+    const long long tiles = static_cast<long long>((kf->width + kTile - 1) / kTile) *
+                            ((kf->height + kTile - 1) / kTile);
+    const long long mine = (tiles + v->cfg.shard_count - 1) / v->cfg.shard_count;
+    const int grid = static_cast<int>(std::max(1LL, std::min<long long>(mine, v->fp_grid_cap)));
+    ProfScope ps(v, 2);
+    launch(k_route, grid, 256, 0, v->stream, fp, r);
+    if (v->profiling) v->prof_launches += 1;
+  }
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));  // peers read after the callers' barrier
+  v->route_nops = n;
+  return RF_OK;
+}
+
 rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
                       int64_t* new_keys_host, int64_t cap, int64_t* n_new) {
   if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
@@ -1006,6 +1172,8 @@ rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
     if (sst != RF_OK) return sst;
     kf = staged.data();
   }
+  if (route_expect(v, 1) != RF_OK) return RF_INVALID_ARG;
+  RouteConsume rc{v};
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -1029,6 +1197,8 @@ rf_status rf_integrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
     if (sst != RF_OK) return sst;
     kf = staged.data();
   }
+  if (route_expect(v, 1) != RF_OK) return RF_INVALID_ARG;
+  RouteConsume rc{v};
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -1056,6 +1226,8 @@ rf_status rf_deintegrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose
     if (sst != RF_OK) return sst;
     kf = staged.data();
   }
+  if (route_expect(v, 1) != RF_OK) return RF_INVALID_ARG;
+  RouteConsume rc{v};
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
@@ -1090,6 +1262,9 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
   r.failed_entry = -1;
   r.failed_phase = -1;
   r.failed_window = -1;
+  // routed: per window, its m removal footprints then its m integration ones
+  if (route_expect(v, static_cast<int>(2 * total)) != RF_OK) return RF_INVALID_ARG;
+  RouteConsume rc{v};
   Batch b;
   // per window: stream(old0) + m x (stream, deint) + stream(new0) + m x (stream, int) + gc
   rf_status st = batch_begin(v, b, static_cast<int>(4 * total + 3 * n_windows + 1));
@@ -1171,6 +1346,7 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     if (st != RF_OK) return st;
     for (int i = 0; i < bad.entry; ++i) {
       op_stream(rb, old_poses[wbase + i].t);
+      rb.route_force = static_cast<int>(2 * wbase + i);  // routed: the removal's footprint
       op_fuse(rb, &staged[i], &old_poses[wbase + i], 0, i);
     }
     BatchOutcome ro;
@@ -1510,9 +1686,12 @@ rf_status rf_profile_end(rf_volume* v, rf_profile* out) {
     } else if (e.kind == 1) {
       p.check_launches++;
       p.check_ms += ms;
-    } else {
+    } else if (e.kind == 2) {
       p.footprint_launches++;
       p.footprint_ms += ms;
+    } else {
+      p.other_launches++;
+      p.other_ms += ms;
     }
     v->event_pool.push_back(e.a);
     v->event_pool.push_back(e.b);

@@ -20,6 +20,7 @@ is where the data lives:
 """
 
 import ctypes
+import threading
 import os
 import struct
 from dataclasses import dataclass, field
@@ -246,6 +247,7 @@ class TwoTierStore:
         self._ptr = None
         self._cfg = None
         self._pending = None  # blocks loaded before the store was bound
+        self._router = None   # routed footprints (connect_shards*)
 
     # -- binding ------------------------------------------------------------
     def _bind(self, cfg):
@@ -285,17 +287,32 @@ class TwoTierStore:
     def config(self):
         return self._cfg
 
-    def _call(self, name, *args):
+    def _call_status(self, name, *args):
         torch = _torch()
         lib = L.lib()
         if torch.cuda.current_device() == self.device:  # the common case: no context switch
             lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
-            st = getattr(lib, name)(self._ptr, *args)
-        else:
-            with torch.cuda.device(self.device):
-                lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
-                st = getattr(lib, name)(self._ptr, *args)
+            return getattr(lib, name)(self._ptr, *args)
+        with torch.cuda.device(self.device):
+            lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
+            return getattr(lib, name)(self._ptr, *args)
+
+    def _call(self, name, *args):
+        _check(self._ptr, self._call_status(name, *args), name)
+
+    def _routed_call(self, name, n_ops, views, poses, centers, *args):
+        """A footprint op of a routed shard: route this call's footprints to
+        their owners, wait for every shard to have routed, run the op, then
+        agree on failure (an error on any shard raises on all of them)."""
+        r = self._router
+        st = self._call_status("rf_route", n_ops, views, poses, centers)
+        r.barrier()  # every shard's footprints are in the inboxes
+        if st == L.RF_OK:
+            st = self._call_status(name, *args)
+        worst = r.agree(st)
         _check(self._ptr, st, name)
+        if worst != L.RF_OK:
+            _check(None, worst, f"{name} (on another shard)")
 
     def close(self):
         if self._ptr is not None:
@@ -472,8 +489,13 @@ def allocate_blocks(store, kf, pose, cfg):
     cap = max(1, store.block_capacity)
     new = np.zeros(min(cap, 1 << 22), dtype=np.int64)
     n = ctypes.c_int64()
-    store._call("rf_allocate", ctypes.byref(view), ctypes.byref(ps),
-                new.ctypes.data_as(L.c_int64_p), len(new), ctypes.byref(n))
+    if store._router is not None:
+        store._routed_call("rf_allocate", 1, ctypes.byref(view), ctypes.byref(ps), None,
+                           ctypes.byref(view), ctypes.byref(ps),
+                           new.ctypes.data_as(L.c_int64_p), len(new), ctypes.byref(n))
+    else:
+        store._call("rf_allocate", ctypes.byref(view), ctypes.byref(ps),
+                    new.ctypes.data_as(L.c_int64_p), len(new), ctypes.byref(n))
     del keep
     return set(keys_to_coords(new[: int(n.value)]))
 
@@ -485,8 +507,13 @@ def integrate(store, kf, pose, cfg):
     ps = pose_struct(pose)
     res = L.RfOpResult()
     new = np.zeros(min(max(1, store.block_capacity), 1 << 22), dtype=np.int64)
-    store._call("rf_integrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res),
-                new.ctypes.data_as(L.c_int64_p), len(new))
+    if store._router is not None:
+        store._routed_call("rf_integrate", 1, ctypes.byref(view), ctypes.byref(ps), None,
+                           ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res),
+                           new.ctypes.data_as(L.c_int64_p), len(new))
+    else:
+        store._call("rf_integrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res),
+                    new.ctypes.data_as(L.c_int64_p), len(new))
     del keep
     return IntegrationRecord(
         kf=kf,
@@ -503,7 +530,11 @@ def deintegrate(store, kf, pose, cfg):
     view, keep = kf_view(kf, store.device)
     ps = pose_struct(pose)
     res = L.RfOpResult()
-    store._call("rf_deintegrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res))
+    if store._router is not None:
+        store._routed_call("rf_deintegrate", 1, ctypes.byref(view), ctypes.byref(ps), None,
+                           ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res))
+    else:
+        store._call("rf_deintegrate", ctypes.byref(view), ctypes.byref(ps), ctypes.byref(res))
     del keep
 
 
@@ -547,6 +578,30 @@ def correct_windows(store, windows, cfg, next_center=None):
     (rf_correct_windows) and ONE host synchronisation for all of them.
     Advances entry.integrated_pose exactly where the sequential reference
     calls would have; raises the reference's exceptions."""
+    if store._router is None:
+        return _correct_windows(store, windows, cfg, next_center)
+    # routed shards: as many windows per native call as the inboxes hold
+    # (every shard makes the same split)
+    per = store._router.max_ops // 2
+    windows = [list(w) for w in windows]
+    if any(len(w) > per for w in windows):
+        raise ValueError(f"a window of more than {per} entries exceeds the routed inboxes "
+                         f"(connect_shards max_ops={store._router.max_ops})")
+    chunks, cur, used = [], [], 0
+    for w in windows:
+        if cur and used + len(w) > per:
+            chunks.append(cur)
+            cur, used = [], 0
+        cur.append(w)
+        used += len(w)
+    chunks.append(cur)
+    done = 0
+    for ci, ch in enumerate(chunks):
+        done += _correct_windows(store, ch, cfg, next_center if ci == len(chunks) - 1 else None)
+    return done
+
+
+def _correct_windows(store, windows, cfg, next_center=None):
     windows = [list(w) for w in windows]
     entries = [e for w in windows for e in w]
     if not entries:
@@ -572,8 +627,23 @@ def correct_windows(store, windows, cfg, next_center=None):
         nc = nca.ctypes.data_as(L.c_double_p)
     res = L.RfWindowResult()
     try:
-        store._call("rf_correct_windows", len(windows), sizes, views, olds, news, nc,
-                    ctypes.byref(res))
+        if store._router is None:
+            store._call("rf_correct_windows", len(windows), sizes, views, olds, news, nc,
+                        ctypes.byref(res))
+        else:  # per window: its m removal footprints, then its m integration ones
+            nr = 2 * n
+            rv, rp = (L.RfKfView * nr)(), (L.RfPose * nr)()
+            rc = np.empty((nr, 3), dtype=np.float64)
+            j = base = 0
+            for w in windows:
+                for poses in (olds, news):
+                    for i in range(base, base + len(w)):
+                        rv[j], rp[j] = views[i], poses[i]
+                        rc[j] = poses[i].t
+                        j += 1
+                base += len(w)
+            store._routed_call("rf_correct_windows", nr, rv, rp, rc.ctypes.data_as(L.c_double_p),
+                               len(windows), sizes, views, olds, news, nc, ctypes.byref(res))
     except (StreamingContractError, VolumeInconsistencyError, CapacityError):
         for w in windows[: max(res.failed_window, 0)]:
             for e in w:
@@ -593,6 +663,97 @@ def correct_windows(store, windows, cfg, next_center=None):
 def correct_entries(store, entries, cfg, next_center=None):
     """One reintegration._correct_entries window (+ optional next_center)."""
     return correct_windows(store, [entries], cfg, next_center)
+
+
+# ---------------------------------------------------------------------------
+# routed footprints for hash-sharded stores (SURVEY §8e; rf_route in the ABI)
+
+
+class _ShardRouter:
+    """What a routed shard needs between its own calls: a barrier across
+    the shards (after every shard routed a call's footprints into the
+    owners' inboxes) and an agreement on the call's status."""
+
+    def __init__(self, max_ops, barrier, agree):
+        self.max_ops = max_ops
+        self.barrier = barrier
+        self.agree = agree
+
+
+class _ThreadGroup:
+    def __init__(self, n, timeout):
+        self.bar = threading.Barrier(n, timeout=timeout)
+        self.codes = [0] * n
+
+    def agree(self, rank, code):
+        self.codes[rank] = code
+        self.bar.wait()
+        worst = max(self.codes)
+        self.bar.wait()
+        return worst
+
+
+def _route_cap(shards, image=(640, 480)):
+    # a sender's distinct keys per op: at most kTileList (512) per 16x16 tile
+    # it samples (tile overflow is flagged as a capacity error, never lost)
+    tiles = -(-image[0] // 16) * -(-image[1] // 16)
+    return -(-tiles // shards) * 512 + 4096
+
+
+def _route_setup(store, max_ops, cap_keys):
+    inbox, nbytes = ctypes.c_void_p(), ctypes.c_uint64()
+    store._call("rf_route_setup", int(max_ops), int(cap_keys), ctypes.byref(inbox),
+                ctypes.byref(nbytes))
+    return inbox.value
+
+
+def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), timeout=300.0):
+    """Route the footprints of G shard stores living in ONE process (one
+    device or several; each shard is then driven from its own thread, e.g.
+    tests and single-process drivers).  Every integrate / deintegrate /
+    allocate_blocks / correct_windows of a shard waits for the other shards'
+    matching call, so the shards must be driven in lockstep."""
+    G = len(stores)
+    if G < 2 or any(s.shard_count != G for s in stores) or \
+            sorted(s.shard_rank for s in stores) != list(range(G)):
+        raise ValueError("connect_shards needs one store per shard rank 0..G-1")
+    cap = cap_keys or _route_cap(G, image)
+    for s in stores:
+        s._bind(cfg)
+    inbox = {s.shard_rank: _route_setup(s, max_ops, cap) for s in stores}
+    arr = (ctypes.c_void_p * G)(*[inbox[r] for r in range(G)])
+    group = _ThreadGroup(G, timeout)
+    for s in stores:
+        s._call("rf_route_connect", arr)
+        s._router = _ShardRouter(max_ops, group.bar.wait,
+                                 (lambda rank: lambda code: group.agree(rank, code))(s.shard_rank))
+
+
+def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640, 480),
+                               group=None):
+    """One shard per process (one GPU each) under torch.distributed: the
+    inboxes are exchanged once as CUDA IPC handles; the per-call barrier and
+    status agreement are torch.distributed collectives."""
+    import torch
+    import torch.distributed as dist
+
+    G = store.shard_count
+    cap = cap_keys or _route_cap(G, image)
+    store._bind(cfg)
+    _route_setup(store, max_ops, cap)
+    h = (ctypes.c_char * 64)()
+    store._call("rf_route_ipc_handle", h)
+    handles = [None] * G
+    dist.all_gather_object(handles, bytes(h), group=group)
+    store._call("rf_route_ipc_open", ctypes.c_char_p(b"".join(handles)))
+    dev = torch.device("cuda", store.device)
+
+    def agree(code):
+        t = torch.tensor([int(code)], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return int(t.item())
+
+    store._router = _ShardRouter(max_ops, lambda: dist.barrier(group=group), agree)
 
 
 # ---------------------------------------------------------------------------
