@@ -8,6 +8,11 @@ protocol the B200 kernels implement:
 * a de-integration's failing key is the MIN over shards (one all_reduce
   per de-integration), and blocks below it are removed + re-added.
 
+* routed footprints (k_route / rf_route): each rank samples only the pixel
+  tiles t with t mod G == rank, keys go to their owners (all-to-all) and
+  the minimum violating key to every rank -- the same volume, including
+  the partial allocation a contract error leaves behind.
+
 Each rank runs the CPU oracle restricted to its own blocks; the union of
 the ranks' volumes must equal the unsharded oracle bit for bit."""
 
@@ -44,38 +49,77 @@ def test_owner_matches_c_abi():
 
 
 class ShardModel:
-    """The oracle volume restricted to one shard's blocks."""
+    """The oracle volume restricted to one shard's blocks.  routed: the
+    footprint is built as k_route builds it -- this rank samples only the
+    16x16 pixel tiles t with t mod G == rank, sends every key to its owner
+    (all-to-all) and the minimum violating key to everyone (all_reduce)."""
 
-    def __init__(self, O, vs, mu, radius, rank, shards):
+    def __init__(self, O, vs, mu, radius, rank, shards, routed=False):
         self.O = O
         self.st = O.OracleStore(vs, mu, radius)
         self.rank, self.G = rank, shards
+        self.routed = routed
 
     def mine(self, coord):
         return owner(int(self.O.pack_coords(*coord)), self.G) == self.rank
 
-    def _allocate(self, coords):
+    def _routed_footprint(self, kf, pose):
+        import torch
+
+        O, st = self.O, self.st
+        intr = kf.intrinsics
+        tiles_x = -(-intr.width // 16)
+        v, u = np.mgrid[0:intr.height, 0:intr.width]
+        tile = (v // 16) * tiles_x + (u // 16)
+        w = np.where(tile % self.G == self.rank, kf.weight, 0.0)  # my pixels only
+        keys = O.footprint_keys(kf.depth, w, intr, pose.rotation, pose.translation,
+                                st.voxel_size, st.mu)
+        big = (1 << 63) - 1
+        bad = [int(k) for k in keys
+               if st.last_center is None or st._center_distance(O.keys_to_coords([k])[0])
+               > st.stream_radius]
+        out = [[int(k) for k in keys if owner(k, self.G) == o] for o in range(self.G)]
+        inbox = [None] * self.G
+        gathered = [None] * self.G  # the all-to-all, as an all-gather on gloo
+        dist.all_gather_object(gathered, out)
+        for src in range(self.G):
+            inbox[src] = gathered[src][self.rank]
+        t = torch.tensor([min(bad) if bad else big], dtype=torch.int64)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        mine = sorted(set(k for seg in inbox for k in seg))
+        return O.keys_to_coords(np.array(mine, dtype=np.int64)), int(t.item())
+
+    def _footprint(self, kf, pose):
+        """(this shard's coords in sorted order, first violating key or None)"""
+        if self.routed:
+            coords, bad = self._routed_footprint(kf, pose)
+            return coords, (None if bad == (1 << 63) - 1 else bad)
+        coords = self.st.footprint(kf, pose)
         st = self.st
         if coords and st.last_center is None:
             raise self.O.StreamingContractError("no sphere")
         first_bad = next((c for c in coords if st._center_distance(c) > st.stream_radius), None)
-        for c in coords:
-            if c == first_bad:
-                raise self.O.StreamingContractError(str(c))
-            if self.mine(c) and c not in st.active:
-                st.active[c] = self.O.Block()
+        bad = None if first_bad is None else int(self.O.pack_coords(*first_bad))
+        return [c for c in coords if self.mine(c)], bad
+
+    def _allocate_mine(self, mine, bad):
+        for c in mine:
+            if bad is not None and int(self.O.pack_coords(*c)) >= bad:
+                break
+            if c not in self.st.active:
+                self.st.active[c] = self.O.Block()
+        if bad is not None:
+            raise self.O.StreamingContractError(str(bad))
 
     def integrate(self, kf, pose):
-        coords = self.st.footprint(kf, pose)
-        self._allocate(coords)
-        for c in coords:
-            if self.mine(c):
-                self.st._fuse(self.st.active[c], c, kf, pose, False)
+        mine, bad = self._footprint(kf, pose)
+        self._allocate_mine(mine, bad)
+        for c in mine:
+            self.st._fuse(self.st.active[c], c, kf, pose, False)
 
     def deintegrate(self, kf, pose):
-        coords = self.st.footprint(kf, pose)
-        self._allocate(coords)
-        mine = [c for c in coords if self.mine(c)]
+        mine, bad = self._footprint(kf, pose)
+        self._allocate_mine(mine, bad)
         local_fail = None
         for c in mine:  # check phase, sorted order
             trial = self.st.active[c].copy()
@@ -99,7 +143,7 @@ class ShardModel:
             raise self.O.VolumeInconsistencyError("negative weight")
 
 
-def _worker(rank, world, port, result_path):
+def _worker(rank, world, port, result_path, routed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle as O
@@ -110,7 +154,7 @@ def _worker(rank, world, port, result_path):
     pose = S.SPose(S.rot_y(0.2), [0.1, -0.05, 0.02])
     wrong = S.SPose(np.eye(3), [1.0, 0.0, 0.0])
     events = []
-    m = ShardModel(O, 0.01, 0.06, 4.0, rank, world)
+    m = ShardModel(O, 0.01, 0.06, 4.0, rank, world, routed)
     m.st.stream(pose.translation)
     for f in frames:
         m.integrate(f, pose)
@@ -119,9 +163,17 @@ def _worker(rank, world, port, result_path):
         m.deintegrate(frames[1], wrong)
     except O.VolumeInconsistencyError:
         events.append("inconsistent")
+    far = np.asarray(pose.translation) + np.array([-2.4, 0.0, 0.0])
+    moved = S.SPose(S.rot_y(0.5), np.asarray(pose.translation) + np.array([0.3, 0.0, 0.0]))
+    m.st.stream(far)
+    try:  # part of the footprint lies outside the sphere: partial allocation
+        m.integrate(frames[2], moved)
+    except O.StreamingContractError:
+        events.append("contract")
+    partial = m.st.export()
     m.st.garbage_collect()
     parts = [None] * world
-    dist.all_gather_object(parts, (m.st.export(), events))
+    dist.all_gather_object(parts, (m.st.export(), events, partial))
     if rank == 0:
         ref = O.OracleStore(0.01, 0.06, 4.0)
         ref.stream(pose.translation)
@@ -133,6 +185,14 @@ def _worker(rank, world, port, result_path):
             ref.deintegrate(frames[1], wrong)
         except O.VolumeInconsistencyError:
             ref_events.append("inconsistent")
+        ref.stream(far)
+        n_alloc = len(ref.active)
+        try:
+            ref.integrate(frames[2], moved)
+        except O.StreamingContractError:
+            ref_events.append("contract")
+        ok_partial = len(ref.active) > n_alloc  # the case allocates before it raises
+        want_partial = ref.export()
         ref.garbage_collect()
         want = ref.export()
         keys = np.concatenate([p[0][0] for p in parts])
@@ -142,6 +202,13 @@ def _worker(rank, world, port, result_path):
             got = np.concatenate([p[0][i] for p in parts])[order]
             ok = ok and np.array_equal(got, want[i])
         ok = ok and all(p[1] == ref_events for p in parts)
+        ok = ok and ref_events == ["inconsistent", "contract"] and ok_partial
+        pk = np.concatenate([p[2][0] for p in parts])
+        po = np.argsort(pk)
+        ok = ok and np.array_equal(pk[po], want_partial[0])
+        for i in (1, 2, 3):
+            ok = ok and np.array_equal(np.concatenate([p[2][i] for p in parts])[po],
+                                       want_partial[i])
         with open(result_path, "w") as fh:
             fh.write("ok" if ok else "mismatch")
     dist.barrier()
@@ -157,4 +224,12 @@ def _free_port():
 def test_two_rank_gloo_sharded_oracle_equals_unsharded(tmp_path):
     out = tmp_path / "result.txt"
     mp.spawn(_worker, args=(2, _free_port(), str(out)), nprocs=2, join=True)
+    assert out.read_text() == "ok"
+
+
+def test_two_rank_gloo_routed_footprints_equal_unsharded(tmp_path):
+    """k_route's protocol: each rank samples half of the pixel tiles, keys go
+    to their owners, the violating key is reduced -- same volume."""
+    out = tmp_path / "result.txt"
+    mp.spawn(_worker, args=(2, _free_port(), str(out), True), nprocs=2, join=True)
     assert out.read_text() == "ok"
