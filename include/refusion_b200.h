@@ -198,6 +198,13 @@ rf_status rf_counters_get(rf_volume *vol, rf_counters *out);
 /* keys [n], data [n][5][512] doubles (D, W, C0, C1, C2); slot order. */
 rf_status rf_export_blocks(rf_volume *vol, int64_t *keys_host, double *data_host,
                            int64_t cap, int64_t *n_out);
+/* marching_cubes (meshing.py:216-245) on the device: vertices and colors
+ * [nv][3] doubles, triangles [nt][3] int64, in the reference's order (blocks
+ * by sorted coordinate, cells by voxel index, cut edges by edge index).
+ * *nv / *nt always receive the sizes; the arrays are written only when all
+ * three are non-NULL and large enough (call once with NULL to size them). */
+rf_status rf_marching_cubes(rf_volume *vol, double *vertices, double *colors, int64_t *triangles,
+                            int64_t vcap, int64_t tcap, int64_t *nv, int64_t *nt);
 /* insert blocks with the given contents (load_volume, volume.py:418-442) */
 rf_status rf_import_blocks(rf_volume *vol, const int64_t *keys_host,
                            const double *data_host, int64_t n);

@@ -24,6 +24,9 @@
 #include "refusion_b200.h"
 #include "rf_kernels.cuh"
 #include "rf_fuse_legacy.cuh"
+#include "rf_mesh.cuh"
+
+#include <cub/cub.cuh>
 
 using namespace rf;
 
@@ -1456,6 +1459,89 @@ rf_status rf_export_blocks(rf_volume* v, int64_t* keys_host, double* data_host, 
   cudaFreeAsync(d_list, v->stream);
   RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
   return RF_OK;
+}
+
+
+// ---- marching cubes (meshing.py:216-245) ----------------------------------
+
+rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int64_t* triangles,
+                            int64_t vcap, int64_t tcap, int64_t* nv_out, int64_t* nt_out) {
+  if (!v || !nv_out || !nt_out || vcap < 0 || tcap < 0) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaStream_t st = v->stream;
+  // every block, both tiers (meshing.py:229-231), sorted by key = by coordinate
+  int* d_list = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_list, sizeof(int) * v->T.capacity, st));
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), st);
+  k_list_live<<<v->n_sms * 4, 256, 0, st>>>(v->T, d_list, v->d_u64);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  const long long n = static_cast<long long>(v->h_u64[0]);
+  *nv_out = 0;
+  *nt_out = 0;
+  if (n == 0) {
+    cudaFreeAsync(d_list, st);
+    RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+    return RF_OK;
+  }
+  long long *keys = nullptr, *keys_sorted = nullptr, *cnt = nullptr, *off = nullptr;
+  int* slots_sorted = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&keys, sizeof(long long) * n, st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&keys_sorted, sizeof(long long) * n, st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&slots_sorted, sizeof(int) * n, st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&cnt, sizeof(long long) * 2 * (n + 1), st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&off, sizeof(long long) * 2 * (n + 1), st));
+  k_gather_keys<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(v->T, d_list, n, keys);
+  size_t tmp_sort = 0, tmp_scan = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, keys, keys_sorted, d_list, slots_sorted,
+                                  static_cast<int>(n), 0, 63, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, cnt, off, static_cast<int>(n + 1), st);
+  void* tmp = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&tmp, std::max(tmp_sort, tmp_scan), st));
+  cub::DeviceRadixSort::SortPairs(tmp, tmp_sort, keys, keys_sorted, d_list, slots_sorted,
+                                  static_cast<int>(n), 0, 63, st);
+  // per-block counts -> exclusive offsets (entry n holds the totals)
+  long long* nv = cnt;
+  long long* nt = cnt + (n + 1);
+  cudaMemsetAsync(cnt, 0, sizeof(long long) * 2 * (n + 1), st);
+  const int grid = static_cast<int>(std::min<long long>(n, 1LL << 20));
+  k_mesh_count<<<grid, kMcThreads, 0, st>>>(v->T, keys_sorted, slots_sorted, n, nv, nt);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_scan, nv, off, static_cast<int>(n + 1), st);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_scan, nt, off + (n + 1), static_cast<int>(n + 1), st);
+  long long tot[2] = {0, 0};
+  cudaMemcpyAsync(&tot[0], off + n, sizeof(long long), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&tot[1], off + (n + 1) + n, sizeof(long long), cudaMemcpyDeviceToHost, st);
+  rf_status rs = RF_OK;
+  if (cudaStreamSynchronize(st) != cudaSuccess) rs = RF_CUDA;
+  *nv_out = tot[0];
+  *nt_out = tot[1];
+  if (rs == RF_OK && vertices && colors && triangles && tot[0] <= vcap && tot[1] <= tcap &&
+      tot[0] > 0) {
+    double *dv = nullptr, *dc = nullptr;
+    long long* dt = nullptr;
+    if (cudaMallocAsync(&dv, sizeof(double) * 3 * tot[0], st) != cudaSuccess ||
+        cudaMallocAsync(&dc, sizeof(double) * 3 * tot[0], st) != cudaSuccess ||
+        cudaMallocAsync(&dt, sizeof(long long) * 3 * std::max(tot[1], 1LL), st) != cudaSuccess) {
+      rs = RF_CAPACITY;
+    } else {
+      k_mesh_emit<<<grid, kMcThreads, 0, st>>>(v->T, keys_sorted, slots_sorted, n, off,
+                                               off + (n + 1), v->cfg.voxel_size, dv, dc, dt);
+      cudaMemcpyAsync(vertices, dv, sizeof(double) * 3 * tot[0], cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(colors, dc, sizeof(double) * 3 * tot[0], cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(triangles, dt, sizeof(long long) * 3 * tot[1], cudaMemcpyDeviceToHost, st);
+    }
+    if (dv) cudaFreeAsync(dv, st);
+    if (dc) cudaFreeAsync(dc, st);
+    if (dt) cudaFreeAsync(dt, st);
+  }
+  for (void* p : {static_cast<void*>(d_list), static_cast<void*>(keys),
+                  static_cast<void*>(keys_sorted), static_cast<void*>(slots_sorted),
+                  static_cast<void*>(cnt), static_cast<void*>(off), tmp})
+    cudaFreeAsync(p, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess)
+    return fail(v, RF_CUDA, "marching cubes failed");
+  if (rs == RF_CAPACITY) return fail(v, RF_CAPACITY, "marching cubes: device memory for the mesh");
+  return rs;
 }
 
 rf_status rf_import_blocks(rf_volume* v, const int64_t* keys_host, const double* data_host,

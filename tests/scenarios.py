@@ -326,3 +326,49 @@ def run_script(adapter, cfg, frames, poses, ops):
         rec["counters"] = [int(x) for x in adapter.counters(store)]
         log.append(rec)
     return log
+
+
+# ---------------------------------------------------------------------------
+# marching cubes (meshing.py:112-245)
+
+
+def mesh_volume(seed=5, voxel=0.01):
+    """A deterministic block set around two spheres: D = signed distance,
+    W > 0 except a few seeded holes (unobserved corners), C a smooth colour
+    ramp; some blocks of the shell are left out (absent +axis neighbours),
+    coordinates straddle zero, and exact zeros / equal corner pairs occur
+    (t = 0 and the midpoint rule).  Returns (keys, data[n][5][512], host_mask)
+    with host_mask marking blocks the reference keeps in its host tier."""
+    rng = np.random.default_rng(seed)
+    span = 8 * voxel
+    centres = [np.array([0.013, -0.021, 0.047]), np.array([-0.09, 0.05, 0.0])]
+    radii = [0.075, 0.045]
+    coords = set()
+    for c, r in zip(centres, radii):
+        lo = np.floor((c - r - 2 * voxel) / span).astype(int)
+        hi = np.floor((c + r + 2 * voxel) / span).astype(int)
+        for bx in range(lo[0], hi[0] + 1):
+            for by in range(lo[1], hi[1] + 1):
+                for bz in range(lo[2], hi[2] + 1):
+                    coords.add((bx, by, bz))
+    coords = sorted(coords)
+    drop = rng.random(len(coords)) < 0.08
+    coords = [c for c, d in zip(coords, drop) if not d]
+    l = np.arange(512)
+    lx, ly, lz = l & 7, (l >> 3) & 7, l >> 6
+    keys, data = [], []
+    for (bx, by, bz) in coords:
+        p = np.stack([(bx * 8 + lx + 0.5) * voxel, (by * 8 + ly + 0.5) * voxel,
+                      (bz * 8 + lz + 0.5) * voxel], axis=1)
+        d = np.min([np.linalg.norm(p - c, axis=1) - r for c, r in zip(centres, radii)], axis=0)
+        d = np.round(d / voxel * 64) / 64 * voxel   # quantised: exact zeros, equal pairs
+        w = 1.0 + (l % 5) * 0.25
+        w[rng.random(512) < 0.02] = 0.0
+        col = np.stack([200 * p[:, 0] + 100, 150 + 0 * p[:, 1] - 300 * p[:, 1], 90 + 400 * p[:, 2]],
+                       axis=0)
+        blk = np.concatenate([d[None], w[None], col], axis=0)
+        keys.append(((bx + (1 << 20)) << 42) | ((by + (1 << 20)) << 21) | (bz + (1 << 20)))
+        data.append(blk)
+    keys = np.array(keys, dtype=np.int64)
+    host = rng.random(len(keys)) < 0.3
+    return keys, np.array(data), host

@@ -1,0 +1,150 @@
+"""Marching cubes + weld (refusion/meshing.py:112-276).
+
+CPU: the packed triangle table equals the reference's, the numpy oracle
+(oracle/mesh_oracle.py) reproduces the reference's golden meshes bit for bit
+and the host weld reproduces the reference's welded meshes.  GPU: the device
+marching cubes (rf_marching_cubes) equals the golden meshes and the oracle,
+bit for bit, on imported and on integrated volumes."""
+
+import os
+import re
+import sys
+
+import numpy as np
+import pytest
+
+import scenarios as S
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(HERE)
+GOLDEN = np.load(os.path.join(HERE, "golden", "mesh_golden.npz"))
+CASES = (("a", 5, 0.01), ("b", 11, 0.004))
+
+
+def oracle():
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import mesh_oracle
+
+    return mesh_oracle
+
+
+def test_packed_table_matches_reference():
+    ref = None
+    for p in (os.path.join(REPO, "oracle", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "refusion")):
+            sys.path.insert(0, p)
+            from refusion import mc_tables as ref
+            break
+    if ref is None:
+        pytest.skip("reference package not present (GPU box)")
+    O = oracle()
+    assert np.array_equal(O.CASE_TRIANGLES, ref.CASE_TRIANGLES)
+    assert np.array_equal(O.CASE_EDGES, ref.CASE_EDGES)
+    assert np.array_equal(O.EDGES, ref.EDGE_VERTEX_PAIRS)
+
+
+@pytest.mark.parametrize("name,seed,voxel", CASES)
+def test_oracle_matches_reference_golden(name, seed, voxel):
+    keys, data, _ = S.mesh_volume(seed, voxel)
+    v, c, t = oracle().marching_cubes(keys, data, voxel)
+    assert np.array_equal(v, GOLDEN[f"{name}_vertices"])
+    assert np.array_equal(c, GOLDEN[f"{name}_colors"])
+    assert np.array_equal(t, GOLDEN[f"{name}_triangles"])
+
+
+@pytest.mark.parametrize("name", [c[0] for c in CASES])
+def test_weld_matches_reference_golden(name):
+    from paper_1709_03763_b200 import meshing as M
+
+    mesh = M.TriangleMesh(GOLDEN[f"{name}_vertices"], GOLDEN[f"{name}_colors"],
+                          GOLDEN[f"{name}_triangles"])
+    mesh.validate()
+    w = M.weld(mesh, 1e-7)
+    assert np.array_equal(w.vertices, GOLDEN[f"{name}_weld_vertices"])
+    assert np.array_equal(w.triangles, GOLDEN[f"{name}_weld_triangles"])
+    with pytest.raises(ValueError):
+        M.weld(mesh, 0.0)
+    assert M.weld(M.TriangleMesh(), 1e-7).n_vertices == 0
+
+
+def test_mesh_writers(tmp_path):
+    from paper_1709_03763_b200 import meshing as M
+
+    mesh = M.TriangleMesh(GOLDEN["a_vertices"], GOLDEN["a_colors"], GOLDEN["a_triangles"])
+    M.save_ply(mesh, tmp_path / "m.ply")
+    raw = (tmp_path / "m.ply").read_bytes()
+    head = raw[: raw.index(b"end_header\n") + len(b"end_header\n")]
+    assert f"element vertex {mesh.n_vertices}".encode() in head
+    assert len(raw) - len(head) == mesh.n_vertices * 15 + mesh.n_triangles * 13
+    M.save_obj(mesh, tmp_path / "m.obj")
+    lines = (tmp_path / "m.obj").read_text().splitlines()
+    assert len(lines) == mesh.n_vertices + mesh.n_triangles
+
+
+# ---------------------------------------------------------------------------
+# device
+
+
+@pytest.fixture(scope="module")
+def V():
+    import torch
+
+    torch.cuda.set_device(0)
+    from paper_1709_03763_b200 import volume
+
+    return volume
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,seed,voxel", CASES)
+def test_device_mc_matches_reference_golden(V, name, seed, voxel):
+    from paper_1709_03763_b200 import meshing as M
+
+    keys, data, _ = S.mesh_volume(seed, voxel)
+    cfg = V.VolumeConfig(voxel_size=voxel, hash_buckets=1 << 12)
+    store = V.TwoTierStore(block_capacity=4096)
+    store._bind(cfg)
+    store._import(keys, data)
+    mesh = M.marching_cubes(store, cfg)
+    mesh.validate()
+    assert np.array_equal(mesh.vertices, GOLDEN[f"{name}_vertices"])
+    assert np.array_equal(mesh.colors, GOLDEN[f"{name}_colors"])
+    assert np.array_equal(mesh.triangles, GOLDEN[f"{name}_triangles"])
+    w = M.weld(mesh, 1e-7)
+    assert np.array_equal(w.triangles, GOLDEN[f"{name}_weld_triangles"])
+
+
+@pytest.mark.gpu
+def test_device_mc_matches_oracle_on_integrated_volume(V):
+    """A volume the device fused from noisy wall frames (negative and positive
+    coordinates, holes): device mesh == oracle mesh of the exported blocks."""
+    from paper_1709_03763_b200 import meshing as M
+
+    rng = np.random.default_rng(8)
+    cfg = V.VolumeConfig(voxel_size=0.005, mu=0.03, stream_radius=6.0, hash_buckets=1 << 14)
+    store = V.TwoTierStore(block_capacity=1 << 15)
+    V.stream(store, np.zeros(3), cfg)
+    for i in range(3):
+        f = S.wall_frame(S.QVGA_INTR, 0.9 + 0.1 * i, rng=rng, tilt=0.3 * i, noise=0.002,
+                         holes=0.05)
+        V.integrate(store, f, S.SPose(S.rot_y(0.1 * i), [0.05 * i - 0.05, 0.02, -0.1]), cfg)
+    keys, d, w, c = store.export()
+    data = np.concatenate([d[:, None], w[:, None], np.transpose(c, (0, 2, 1))], axis=1)
+    v, col, t = oracle().marching_cubes(keys, data, cfg.voxel_size)
+    mesh = M.marching_cubes(store, cfg)
+    assert mesh.n_triangles > 1000
+    assert np.array_equal(mesh.vertices, v)
+    assert np.array_equal(mesh.colors, col)
+    assert np.array_equal(mesh.triangles, t)
+
+
+@pytest.mark.gpu
+def test_device_mc_empty(V):
+    from paper_1709_03763_b200 import meshing as M
+
+    cfg = V.VolumeConfig(voxel_size=0.01, hash_buckets=1 << 10)
+    store = V.TwoTierStore(block_capacity=64)
+    mesh = M.marching_cubes(store, cfg)
+    assert mesh.n_vertices == 0 and mesh.n_triangles == 0
+    store.put_block((0, 0, 0), d=np.ones(512), w=np.ones(512))  # no sign change
+    assert M.marching_cubes(store, cfg).n_triangles == 0
