@@ -205,6 +205,12 @@ rf_status rf_export_blocks(rf_volume *vol, int64_t *keys_host, double *data_host
  * three are non-NULL and large enough (call once with NULL to size them). */
 rf_status rf_marching_cubes(rf_volume *vol, double *vertices, double *colors, int64_t *triangles,
                             int64_t vcap, int64_t tcap, int64_t *nv, int64_t *nt);
+/* nn_min_d2 (_kernels_cy.pyx:111-129; refusion.kernels.nn_min_d2): out[i] =
+ * min_j (dx*dx + dy*dy) + dz*dz over pts, q [n][3] / pts [m][3] / out [n]
+ * HOST arrays (copied through the device); +inf when m == 0.  stream may be
+ * NULL.  Needs no volume. */
+rf_status rf_nn_min_d2(const double *q, int64_t n, const double *pts, int64_t m, double *out,
+                       void *stream);
 /* insert blocks with the given contents (load_volume, volume.py:418-442) */
 rf_status rf_import_blocks(rf_volume *vol, const int64_t *keys_host,
                            const double *data_host, int64_t n);

@@ -132,3 +132,20 @@ def marching_cubes(keys, data, voxel_size):
     if not vs:
         return np.zeros((0, 3)), np.zeros((0, 3)), np.zeros((0, 3), dtype=np.int64)
     return np.concatenate(vs), np.concatenate(cs), np.concatenate(ts)
+
+
+def nn_min_d2(q, pts):
+    """_kernels_cy.pyx:111-129 / _kernels_py.py:107-120: per query the minimum
+    of (dx*dx + dy*dy) + dz*dz over the points (+inf without points)."""
+    q = np.asarray(q, dtype=np.float64)
+    pts = np.asarray(pts, dtype=np.float64)
+    out = np.full(len(q), np.inf)
+    for lo in range(0, len(pts), 4096):
+        p = pts[lo:lo + 4096]
+        dx = q[:, None, 0] - p[None, :, 0]
+        dy = q[:, None, 1] - p[None, :, 1]
+        dz = q[:, None, 2] - p[None, :, 2]
+        d2 = dx * dx + dy * dy
+        d2 = d2 + dz * dz
+        np.minimum(out, d2.min(axis=1), out=out)
+    return out

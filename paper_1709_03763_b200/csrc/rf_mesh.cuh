@@ -15,6 +15,8 @@
 
 #include "rf_kernels.cuh"
 
+#include <math_constants.h>
+
 namespace rf {
 
 // Corner i of a cell: (x, y, z) offsets (meshing.py:23-35)
@@ -111,38 +113,6 @@ __device__ __forceinline__ int mc_nb_index(int dx, int dy, int dz) {
   return map[code];
 }
 
-struct McCell {
-  unsigned cube, edges;
-  int n_tri;
-  bool live;
-  double d[8], w[8];
-  int slot[8], voxel[8];
-};
-
-// Corner samples of cell l of the block whose neighbour slots are nb[0..7]
-// (nb[0] the block itself, -1 absent: W = 0, unobserved).
-__device__ __forceinline__ void mc_cell(const Table& T, const int* nb, int l, McCell& c) {
-  const int x = l & 7, y = (l >> 3) & 7, z = l >> 6;
-  bool observed = true;
-  c.cube = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int vx = x + kMcCorner[i][0], vy = y + kMcCorner[i][1], vz = z + kMcCorner[i][2];
-    const int s = nb[mc_nb_index(vx >> 3, vy >> 3, vz >> 3)];
-    const int v = (vx & 7) + 8 * (vy & 7) + 64 * (vz & 7);
-    c.slot[i] = s;
-    c.voxel[i] = v;
-    const double* blk = T.pool + static_cast<size_t>(s < 0 ? 0 : s) * kBlockDoubles;
-    c.d[i] = s < 0 ? 0.0 : blk[v];
-    c.w[i] = s < 0 ? 0.0 : blk[kBlockVoxels + v];
-    observed = observed && c.w[i] > 0.0;
-    c.cube |= (c.d[i] < 0.0 ? 1u : 0u) << i;
-  }
-  c.edges = mc_edge_mask(c.cube);
-  c.live = observed && c.edges != 0;
-  c.n_tri = c.live ? static_cast<int>(kMcTriangles[c.cube] >> 60) : 0;
-}
-
 // The block's own slot and its seven +axis neighbours, looked up once per CTA.
 __device__ __forceinline__ void mc_neighbours(const Table& T, long long key, int slot, int* nb) {
   if (threadIdx.x < 8) {
@@ -164,22 +134,73 @@ __device__ __forceinline__ void mc_neighbours(const Table& T, long long key, int
     }
     nb[threadIdx.x] = s;
   }
-  __syncthreads();
 }
 
-constexpr int kMcThreads = 512;  // one thread per cell
+constexpr int kMcThreads = 128;  // four consecutive cells per thread
+constexpr int kMcCells = kBlockVoxels / kMcThreads;
+constexpr int kMcPad = 9;        // padded corner grid (meshing.py:112-146)
+constexpr int kMcPadN = kMcPad * kMcPad * kMcPad;
+
+// Padded position (x, y, z) in 0..8: owning block (neighbour index) and voxel.
+__device__ __forceinline__ void mc_pad_source(const int* nb, int x, int y, int z, int& slot,
+                                              int& voxel) {
+  slot = nb[mc_nb_index(x >> 3, y >> 3, z >> 3)];
+  voxel = (x & 7) + 8 * (y & 7) + 64 * (z & 7);
+}
+
+// Stage D and W of the 9x9x9 padded grid in shared memory (coalesced along
+// x; an absent neighbour's corners read as W = 0, unobserved).
+__device__ __forceinline__ void mc_stage(const Table& T, const int* nb, double* s_d, double* s_w) {
+  for (int j = threadIdx.x; j < kMcPadN; j += blockDim.x) {
+    int slot, voxel;
+    mc_pad_source(nb, j % kMcPad, (j / kMcPad) % kMcPad, j / (kMcPad * kMcPad), slot, voxel);
+    const double* blk = T.pool + static_cast<size_t>(slot < 0 ? 0 : slot) * kBlockDoubles;
+    s_d[j] = slot < 0 ? 0.0 : blk[voxel];
+    s_w[j] = slot < 0 ? 0.0 : blk[kBlockVoxels + voxel];
+  }
+}
+
+__device__ __forceinline__ int mc_pad_index(int l, int corner) {
+  const int x = (l & 7) + kMcCorner[corner][0], y = ((l >> 3) & 7) + kMcCorner[corner][1],
+            z = (l >> 6) + kMcCorner[corner][2];
+  return (z * kMcPad + y) * kMcPad + x;
+}
+
+// Case of cell l (meshing.py:157-164): 0 when not live.
+__device__ __forceinline__ unsigned mc_case(const double* s_d, const double* s_w, int l,
+                                            bool& live) {
+  unsigned cube = 0;
+  bool observed = true;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int j = mc_pad_index(l, i);
+    observed = observed && s_w[j] > 0.0;
+    cube |= (s_d[j] < 0.0 ? 1u : 0u) << i;
+  }
+  live = observed && mc_edge_mask(cube) != 0;
+  return cube;
+}
 
 // Pass 1: vertices and triangles per block (sorted order).
-__global__ void __launch_bounds__(kMcThreads) k_mesh_count(Table T, const long long* keys,
+__global__ void __launch_bounds__(kMcThreads, 8) k_mesh_count(Table T, const long long* keys,
                                                            const int* slots, long long n,
                                                            long long* nv, long long* nt) {
   __shared__ int nb[8];
+  __shared__ double s_d[kMcPadN], s_w[kMcPadN];
   __shared__ int s_v[kMcThreads / 32], s_t[kMcThreads / 32];
   for (long long b = blockIdx.x; b < n; b += gridDim.x) {
     mc_neighbours(T, keys[b], slots[b], nb);
-    McCell c;
-    mc_cell(T, nb, threadIdx.x, c);
-    int v = c.live ? __popc(c.edges) : 0, t = c.n_tri;
+    __syncthreads();
+    mc_stage(T, nb, s_d, s_w);
+    __syncthreads();
+    int v = 0, t = 0;
+#pragma unroll
+    for (int q = 0; q < kMcCells; ++q) {
+      bool live;
+      const unsigned cube = mc_case(s_d, s_w, threadIdx.x * kMcCells + q, live);
+      v += live ? __popc(mc_edge_mask(cube)) : 0;
+      t += live ? static_cast<int>(kMcTriangles[cube] >> 60) : 0;
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       v += __shfl_xor_sync(kFull, v, o);
@@ -203,30 +224,51 @@ __global__ void __launch_bounds__(kMcThreads) k_mesh_count(Table T, const long l
   }
 }
 
-// Pass 2: write the block's vertices, colours and triangles at its offsets.
-__global__ void __launch_bounds__(kMcThreads) k_mesh_emit(Table T, const long long* keys,
+// Pass 2: the block's vertices, colours and triangles at its offsets.  Each
+// live cell lists its (cell, cut edge) and (cell, triangle) entries in shared
+// memory at its prefix; the CTA then writes the block's contiguous output
+// ranges one vertex / triangle per thread (coalesced stores).
+__global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, const long long* keys,
                                                           const int* slots, long long n,
                                                           const long long* v_off,
                                                           const long long* t_off, double vs,
                                                           double* verts, double* cols,
                                                           long long* tris) {
   __shared__ int nb[8];
+  __shared__ double s_d[kMcPadN], s_w[kMcPadN];
+  __shared__ unsigned short s_vlist[kBlockVoxels * 12];  // cell << 4 | edge
+  __shared__ unsigned short s_tlist[kBlockVoxels * 5];   // cell << 3 | triangle
+  __shared__ int s_vpre[kBlockVoxels];
+  __shared__ unsigned char s_cube[kBlockVoxels];
   __shared__ int s_v[kMcThreads / 32], s_t[kMcThreads / 32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (long long b = blockIdx.x; b < n; b += gridDim.x) {
     const long long key = keys[b];
     mc_neighbours(T, key, slots[b], nb);
-    McCell c;
-    mc_cell(T, nb, threadIdx.x, c);
-    const int nv_cell = c.live ? __popc(c.edges) : 0;
-    // exclusive prefix over cells in l order (warp scan + warp totals)
-    int iv = nv_cell, it = c.n_tri;
+    __syncthreads();
+    mc_stage(T, nb, s_d, s_w);
+    __syncthreads();
+    // this thread's cells l0 .. l0 + kMcCells - 1 (consecutive: l order)
+    const int l0 = threadIdx.x * kMcCells;
+    unsigned cubes[kMcCells];
+    int nvc[kMcCells], ntc[kMcCells], sv = 0, st = 0;
+#pragma unroll
+    for (int q = 0; q < kMcCells; ++q) {
+      bool live;
+      cubes[q] = mc_case(s_d, s_w, l0 + q, live);
+      nvc[q] = live ? __popc(mc_edge_mask(cubes[q])) : 0;
+      ntc[q] = live ? static_cast<int>(kMcTriangles[cubes[q]] >> 60) : 0;
+      sv += nvc[q];
+      st += ntc[q];
+    }
+    // exclusive prefix over threads (warp scan + warp totals)
+    int iv = sv, it = st;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int a = __shfl_up_sync(kFull, iv, o), bt = __shfl_up_sync(kFull, it, o);
+      const int a = __shfl_up_sync(kFull, iv, o), c = __shfl_up_sync(kFull, it, o);
       if (lane >= o) {
         iv += a;
-        it += bt;
+        it += c;
       }
     }
     if (lane == 31) {
@@ -234,50 +276,124 @@ __global__ void __launch_bounds__(kMcThreads) k_mesh_emit(Table T, const long lo
       s_t[warp] = it;
     }
     __syncthreads();
-    int wv = 0, wt = 0;
-    for (int i = 0; i < warp; ++i) {
-      wv += s_v[i];
-      wt += s_t[i];
+    int wv = 0, wt = 0, tv = 0, tt = 0;
+    for (int i = 0; i < kMcThreads / 32; ++i) {
+      if (i < warp) {
+        wv += s_v[i];
+        wt += s_t[i];
+      }
+      tv += s_v[i];
+      tt += s_t[i];
+    }
+    int vpre = wv + iv - sv, tpre = wt + it - st;
+#pragma unroll
+    for (int q = 0; q < kMcCells; ++q) {
+      const int l = l0 + q;
+      s_vpre[l] = vpre;
+      s_cube[l] = static_cast<unsigned char>(cubes[q]);
+      if (nvc[q]) {
+        const unsigned edges = mc_edge_mask(cubes[q]);
+        int r = vpre;
+        for (int e = 0; e < 12; ++e)
+          if ((edges >> e) & 1u) s_vlist[r++] = static_cast<unsigned short>((l << 4) | e);
+        for (int k = 0; k < ntc[q]; ++k)
+          s_tlist[tpre + k] = static_cast<unsigned short>((l << 3) | k);
+      }
+      vpre += nvc[q];
+      tpre += ntc[q];
     }
     __syncthreads();
-    if (c.live) {
-      const long long vbase = v_off[b] + wv + iv - nv_cell;
-      const long long tbase = t_off[b] + wt + it - c.n_tri;
-      long long bx, by, bz;
-      unpack_key(key, bx, by, bz);
-      const int x = threadIdx.x & 7, y = (threadIdx.x >> 3) & 7, z = threadIdx.x >> 6;
+    const long long vb = v_off[b], tb = t_off[b];
+    long long bx, by, bz;
+    unpack_key(key, bx, by, bz);
+    for (int j = threadIdx.x; j < tv; j += kMcThreads) {
+      const int cell = s_vlist[j] >> 4, e = s_vlist[j] & 15;
+      const int a = kMcEdge[e][0], c = kMcEdge[e][1];
+      const double da = s_d[mc_pad_index(cell, a)], db = s_d[mc_pad_index(cell, c)];
+      const double den = da - db;
+      const double t = den == 0.0 ? 0.5 : da / den;  // meshing.py:180-182
+      const int x = cell & 7, y = (cell >> 3) & 7, z = cell >> 6;
       // corner v0 centre: (anchor + 0.5) * vs (meshing.py:190-192)
       const double base[3] = {(static_cast<double>(x + bx * kBlockSide) + 0.5) * vs,
                               (static_cast<double>(y + by * kBlockSide) + 0.5) * vs,
                               (static_cast<double>(z + bz * kBlockSide) + 0.5) * vs};
-      int r = 0;
-      for (int e = 0; e < 12; ++e) {
-        if (!((c.edges >> e) & 1u)) continue;
-        const int a = kMcEdge[e][0], bb = kMcEdge[e][1];
-        const double da = c.d[a], db = c.d[bb];
-        const double den = da - db;
-        const double t = den == 0.0 ? 0.5 : da / den;  // meshing.py:180-182
-        const long long vi = vbase + r++;
+      int sa, va, sc, vc;
+      mc_pad_source(nb, x + kMcCorner[a][0], y + kMcCorner[a][1], z + kMcCorner[a][2], sa, va);
+      mc_pad_source(nb, x + kMcCorner[c][0], y + kMcCorner[c][1], z + kMcCorner[c][2], sc, vc);
+      const double* pa_blk = T.pool + static_cast<size_t>(sa) * kBlockDoubles;
+      const double* pc_blk = T.pool + static_cast<size_t>(sc) * kBlockDoubles;
+      const long long vi = vb + j;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          const double pa = base[k] + (kMcCorner[a][k] ? vs : 0.0);
-          const double pb = base[k] + (kMcCorner[bb][k] ? vs : 0.0);
-          verts[3 * vi + k] = pa + t * (pb - pa);
-          const double* ba = T.pool + static_cast<size_t>(c.slot[a]) * kBlockDoubles;
-          const double* bbp = T.pool + static_cast<size_t>(c.slot[bb]) * kBlockDoubles;
-          const double ca = ba[(2 + k) * kBlockVoxels + c.voxel[a]];
-          const double cb = bbp[(2 + k) * kBlockVoxels + c.voxel[bb]];
-          cols[3 * vi + k] = ca + t * (cb - ca);
-        }
+      for (int k = 0; k < 3; ++k) {
+        const double pa = base[k] + (kMcCorner[a][k] ? vs : 0.0);
+        const double pb = base[k] + (kMcCorner[c][k] ? vs : 0.0);
+        verts[3 * vi + k] = pa + t * (pb - pa);
+        const double ca = pa_blk[(2 + k) * kBlockVoxels + va];
+        const double cb = pc_blk[(2 + k) * kBlockVoxels + vc];
+        cols[3 * vi + k] = ca + t * (cb - ca);
       }
-      const unsigned long long tl = kMcTriangles[c.cube];
-      for (int k = 0; k < 3 * c.n_tri; ++k) {
-        const int e = static_cast<int>((tl >> (4 * k)) & 0xf);
-        tris[3 * tbase + k] = vbase + __popc(c.edges & ((1u << e) - 1u));
+    }
+    for (int j = threadIdx.x; j < tt; j += kMcThreads) {
+      const int cell = s_tlist[j] >> 3, k = s_tlist[j] & 7;
+      const unsigned cb = s_cube[cell];
+      const unsigned em = mc_edge_mask(cb);
+      const unsigned long long tl = kMcTriangles[cb];
+      const long long v0 = vb + s_vpre[cell];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int e = static_cast<int>((tl >> (4 * (3 * k + i))) & 0xf);
+        tris[3 * (tb + j) + i] = v0 + __popc(em & ((1u << e) - 1u));
       }
     }
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------------------
+// nn_min_d2 (the reference plugin's evaluation kernel, _kernels_cy.pyx:111-129):
+// per query the minimum over all points of (dx*dx + dy*dy) + dz*dz, IEEE f64
+// without contraction (the min itself is exact, so the point order is free).
+// Points stream through shared memory in tiles; each thread owns two queries.
+
+constexpr int kNnThreads = 256;
+constexpr int kNnTile = 1024;  // points per shared-memory tile (24 KB)
+
+__global__ void __launch_bounds__(kNnThreads) k_nn_min_d2(const double* __restrict__ q, long long n,
+                                                          const double* __restrict__ pts,
+                                                          long long m, double* __restrict__ out) {
+  __shared__ double sp[3][kNnTile];
+  const long long i0 = (static_cast<long long>(blockIdx.x) * kNnThreads + threadIdx.x) * 2;
+  double qx[2], qy[2], qz[2], best[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const long long i = i0 + k < n ? i0 + k : 0;
+    qx[k] = n ? q[3 * i] : 0.0;
+    qy[k] = n ? q[3 * i + 1] : 0.0;
+    qz[k] = n ? q[3 * i + 2] : 0.0;
+    best[k] = CUDART_INF;
+  }
+  for (long long base = 0; base < m; base += kNnTile) {
+    const int cnt = static_cast<int>(m - base < kNnTile ? m - base : kNnTile);
+    __syncthreads();
+    for (int j = threadIdx.x; j < 3 * cnt; j += kNnThreads) {
+      const double v = pts[3 * base + j];
+      sp[j % 3][j / 3] = v;
+    }
+    __syncthreads();
+    for (int j = 0; j < cnt; ++j) {
+      const double px = sp[0][j], py = sp[1][j], pz = sp[2][j];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double dx = qx[k] - px, dy = qy[k] - py, dz = qz[k] - pz;
+        double d2 = dx * dx + dy * dy;
+        d2 = d2 + dz * dz;
+        best[k] = d2 < best[k] ? d2 : best[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k)
+    if (i0 + k < n) out[i0 + k] = best[k];
 }
 
 }  // namespace rf

@@ -1544,6 +1544,33 @@ rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int6
   return rs;
 }
 
+
+// ---- nn_min_d2 (_kernels_cy.pyx:111-129), the plugin's evaluation kernel ----
+
+rf_status rf_nn_min_d2(const double* q, int64_t n, const double* pts, int64_t m, double* out,
+                       void* stream) {
+  if (n < 0 || m < 0 || (n > 0 && (!q || !out)) || (m > 0 && !pts)) return RF_INVALID_ARG;
+  if (n == 0) return RF_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *dq = nullptr, *dp = nullptr, *dout = nullptr;
+  const size_t bq = sizeof(double) * 3 * n, bp = sizeof(double) * 3 * std::max<int64_t>(m, 1);
+  if (cudaMallocAsync(&dq, bq, st) != cudaSuccess || cudaMallocAsync(&dp, bp, st) != cudaSuccess ||
+      cudaMallocAsync(&dout, sizeof(double) * n, st) != cudaSuccess) {
+    cudaGetLastError();
+    return RF_CAPACITY;
+  }
+  cudaMemcpyAsync(dq, q, bq, cudaMemcpyHostToDevice, st);
+  if (m > 0) cudaMemcpyAsync(dp, pts, sizeof(double) * 3 * m, cudaMemcpyHostToDevice, st);
+  const long long blocks = (n + 2 * kNnThreads - 1) / (2 * kNnThreads);
+  k_nn_min_d2<<<static_cast<unsigned>(blocks), kNnThreads, 0, st>>>(dq, n, dp, m, dout);
+  cudaMemcpyAsync(out, dout, sizeof(double) * n, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(dq, st);
+  cudaFreeAsync(dp, st);
+  cudaFreeAsync(dout, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) return RF_CUDA;
+  return RF_OK;
+}
+
 rf_status rf_import_blocks(rf_volume* v, const int64_t* keys_host, const double* data_host,
                            int64_t n) {
   if (!v || n < 0 || (n > 0 && (!keys_host || !data_host))) return RF_INVALID_ARG;

@@ -2,7 +2,8 @@
 
 ``refusion.kernels`` (/root/reference/pkg/src/refusion/kernels.py:19-41)
 exports ``BACKEND``, ``fuse_block`` and ``nn_min_d2``.  This module exports
-the same names; ``fuse_block`` runs the sm_100a integrate / de-integrate
+the same names; ``nn_min_d2`` (the evaluation metrics' nearest-point scan)
+runs on the device too; ``fuse_block`` runs the sm_100a integrate / de-integrate
 device code on one block (host arrays in, modified in place), with the same
 argument meaning and the same return convention (voxel count, or -1 with
 the block untouched on a removal-consistency failure,
@@ -58,11 +59,18 @@ def fuse_block(d, w, c, ox, oy, oz, voxel_size, rot, tx, ty, tz, fx, fy, cx, cy,
 
 
 def nn_min_d2(q, pts, out):
-    """Off the hot path (evaluation metric): not served by
-    the B200 backend in this round."""
-    raise NotImplementedError(
-        "nn_min_d2 is an evaluation kernel outside the B200 hot path; use the "
-        "reference backend for mesh metrics")
+    """_kernels_cy.pyx:111-129 on the device (rf_nn_min_d2): out[i] = min over
+    pts of (dx*dx + dy*dy) + dz*dz, bit for bit (the min is exact, so the
+    device's point order cannot change it).  Same arguments: C-contiguous
+    float64 q [n, 3], pts [m, 3], out [n], written in place."""
+    n = q.shape[0] if isinstance(q, np.ndarray) else -1
+    m = pts.shape[0] if isinstance(pts, np.ndarray) else -1
+    pq = _f64(q, (n, 3), "q")
+    pp = _f64(pts, (m, 3), "pts")
+    po = _f64(out, (n,), "out")
+    st = L.lib().rf_nn_min_d2(pq, n, pp, m, po, None)
+    if st != L.RF_OK:
+        raise RuntimeError(f"rf_nn_min_d2 failed: {L.lib().rf_status_string(st).decode()}")
 
 
 __all__ = ["BACKEND", "fuse_block", "nn_min_d2"]

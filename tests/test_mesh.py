@@ -148,3 +148,44 @@ def test_device_mc_empty(V):
     assert mesh.n_vertices == 0 and mesh.n_triangles == 0
     store.put_block((0, 0, 0), d=np.ones(512), w=np.ones(512))  # no sign change
     assert M.marching_cubes(store, cfg).n_triangles == 0
+
+
+# ---------------------------------------------------------------------------
+# nn_min_d2: the plugin's evaluation kernel (_kernels_cy.pyx:111-129)
+
+
+def _nn_case(seed, n, m):
+    rng = np.random.default_rng(seed)
+    q = rng.normal(size=(n, 3)) * rng.choice([1e-3, 1.0, 50.0], size=(n, 1))
+    pts = rng.normal(size=(m, 3))
+    if m and n > 4:
+        q[:3] = pts[rng.integers(0, m, 3)]  # exact hits: d2 = 0
+    return np.ascontiguousarray(q), np.ascontiguousarray(pts)
+
+
+def test_nn_oracle_matches_reference_python():
+    ref = None
+    for p in (os.path.join(REPO, "oracle", "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(p, "refusion")):
+            sys.path.insert(0, p)
+            from refusion import _kernels_py as ref
+            break
+    if ref is None:
+        pytest.skip("reference package not present")
+    q, pts = _nn_case(1, 300, 5000)
+    want = np.empty(len(q))
+    ref.nn_min_d2(q, pts, want)
+    assert np.array_equal(oracle().nn_min_d2(q, pts), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,m", [(1, 1), (513, 1), (1000, 3000), (4097, 1025), (7, 0), (0, 5)])
+def test_device_nn_min_d2_matches_oracle(V, n, m):
+    from paper_1709_03763_b200 import kernels as K
+
+    q, pts = _nn_case(n + m, n, m)
+    out = np.empty(n)
+    K.nn_min_d2(q, pts, out)
+    assert np.array_equal(out, oracle().nn_min_d2(q, pts))
+    with pytest.raises((TypeError, ValueError)):
+        K.nn_min_d2(q.astype(np.float32), pts, out)
