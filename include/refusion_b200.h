@@ -205,6 +205,11 @@ rf_status rf_export_blocks(rf_volume *vol, int64_t *keys_host, double *data_host
  * three are non-NULL and large enough (call once with NULL to size them). */
 rf_status rf_marching_cubes(rf_volume *vol, double *vertices, double *colors, int64_t *triangles,
                             int64_t vcap, int64_t tcap, int64_t *nv, int64_t *nt);
+/* marching_cubes followed by weld(mesh, tol) (meshing.py:248-276), both on the
+ * device: the welded mesh only crosses to the host.  Same sizing protocol. */
+rf_status rf_marching_cubes_welded(rf_volume *vol, double tol, double *vertices, double *colors,
+                                   int64_t *triangles, int64_t vcap, int64_t tcap, int64_t *nv,
+                                   int64_t *nt);
 /* nn_min_d2 (_kernels_cy.pyx:111-129; refusion.kernels.nn_min_d2): out[i] =
  * min_j (dx*dx + dy*dy) + dz*dz over pts, q [n][3] / pts [m][3] / out [n]
  * HOST arrays (copied through the device); +inf when m == 0.  stream may be

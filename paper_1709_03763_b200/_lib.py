@@ -186,6 +186,8 @@ SIGNATURES = {
     "rf_import_blocks": (_S, [_vp, c_int64_p, c_double_p, ctypes.c_int64]),
     "rf_nn_min_d2": (_S, [c_double_p, ctypes.c_int64, c_double_p, ctypes.c_int64, c_double_p,
                           _vp]),
+    "rf_marching_cubes_welded": (_S, [_vp, ctypes.c_double, c_double_p, c_double_p, c_int64_p,
+                                      ctypes.c_int64, ctypes.c_int64, c_int64_p, c_int64_p]),
     "rf_marching_cubes": (_S, [_vp, c_double_p, c_double_p, c_int64_p, ctypes.c_int64,
                                ctypes.c_int64, c_int64_p, c_int64_p]),
     "rf_read_blocks": (_S, [_vp, c_int64_p, ctypes.c_int64, c_double_p, c_int32_p]),

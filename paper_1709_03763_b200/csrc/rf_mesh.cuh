@@ -350,6 +350,93 @@ __global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, const long
 }
 
 // ---------------------------------------------------------------------------
+// weld (meshing.py:248-276) on the device: key = rint(v / tol) per axis (numpy's
+// round-half-even), rows sorted lexicographically by a stable LSD radix sort
+// (z, then y, then x keys, carrying the vertex index, so equal keys keep index
+// order and a segment's first entry is its lowest index -- np.unique's
+// return_index), the first vertex of each segment kept, triangles remapped
+// and collapsed ones dropped in order.
+
+__global__ void k_weld_keys(const double* __restrict__ v, long long n, double tol,
+                            long long* __restrict__ kx, long long* __restrict__ ky,
+                            long long* __restrict__ kz, int* __restrict__ idx) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    kx[i] = __double2ll_rn(v[3 * i] / tol);
+    ky[i] = __double2ll_rn(v[3 * i + 1] / tol);
+    kz[i] = __double2ll_rn(v[3 * i + 2] / tol);
+    idx[i] = static_cast<int>(i);
+  }
+}
+
+__global__ void k_weld_gather(const long long* __restrict__ src, const int* __restrict__ perm,
+                              long long n, long long* __restrict__ dst) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    dst[i] = src[perm[i]];
+}
+
+__global__ void k_weld_flags(const long long* __restrict__ kx, const long long* __restrict__ ky,
+                             const long long* __restrict__ kz, const int* __restrict__ perm,
+                             long long n, int* __restrict__ flag) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    int f = 1;
+    if (i > 0) {
+      const int a = perm[i], b = perm[i - 1];
+      f = kx[a] != kx[b] || ky[a] != ky[b] || kz[a] != kz[b];
+    }
+    flag[i] = f;
+  }
+}
+
+// seg = inclusive scan of flag (segment id + 1)
+__global__ void k_weld_scatter(const int* __restrict__ perm, const int* __restrict__ flag,
+                               const int* __restrict__ seg, long long n,
+                               const double* __restrict__ v, const double* __restrict__ c,
+                               double* __restrict__ vo, double* __restrict__ co,
+                               int* __restrict__ inverse) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int src = perm[i], u = seg[i] - 1;
+    inverse[src] = u;
+    if (flag[i]) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        vo[3 * static_cast<long long>(u) + k] = v[3 * static_cast<long long>(src) + k];
+        co[3 * static_cast<long long>(u) + k] = c[3 * static_cast<long long>(src) + k];
+      }
+    }
+  }
+}
+
+__global__ void k_weld_tris(const long long* __restrict__ t, long long nt,
+                            const int* __restrict__ inverse, long long* __restrict__ tr,
+                            int* __restrict__ keep) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nt;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long a = inverse[t[3 * i]], b = inverse[t[3 * i + 1]], c = inverse[t[3 * i + 2]];
+    tr[3 * i] = a;
+    tr[3 * i + 1] = b;
+    tr[3 * i + 2] = c;
+    keep[i] = a != b && b != c && a != c;
+  }
+}
+
+// pos = inclusive scan of keep
+__global__ void k_weld_compact(const long long* __restrict__ tr, const int* __restrict__ keep,
+                               const int* __restrict__ pos, long long nt,
+                               long long* __restrict__ out) {
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < nt;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    if (!keep[i]) continue;
+    const long long o = pos[i] - 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) out[3 * o + k] = tr[3 * i + k];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // nn_min_d2 (the reference plugin's evaluation kernel, _kernels_cy.pyx:111-129):
 // per query the minimum over all points of (dx*dx + dy*dy) + dz*dz, IEEE f64
 // without contraction (the min itself is exact, so the point order is free).

@@ -1464,8 +1464,79 @@ rf_status rf_export_blocks(rf_volume* v, int64_t* keys_host, double* data_host, 
 
 // ---- marching cubes (meshing.py:216-245) ----------------------------------
 
-rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int64_t* triangles,
-                            int64_t vcap, int64_t tcap, int64_t* nv_out, int64_t* nt_out) {
+}  // extern "C"
+
+namespace {
+
+// Device weld of (dv, dc, dt) (meshing.py:248-276); on success the outputs
+// replace the inputs (caller frees the returned buffers).
+rf_status weld_device(rf_volume* v, double tol, double*& dv, double*& dc, long long*& dt,
+                      long long& nv, long long& nt) {
+  cudaStream_t st = v->stream;
+  if (nv >= (1LL << 31) || nt >= (1LL << 31)) return RF_CAPACITY;
+  const int n = static_cast<int>(nv), m = static_cast<int>(nt);
+  const int g = v->n_sms * 8;
+  long long *kx, *ky, *kz, *kg, *ks, *tr, *to;
+  int *ia, *ib, *flag, *seg, *inv, *keep, *pos;
+  double *vo, *co;
+  void* tmp = nullptr;
+  size_t t_sort = 0, t_scan = 0, t_scan2 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (long long*)nullptr, (long long*)nullptr,
+                                  (int*)nullptr, (int*)nullptr, n, 0, 64, st);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan, (int*)nullptr, (int*)nullptr, n, st);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan2, (int*)nullptr, (int*)nullptr, std::max(m, 1), st);
+  const size_t bn = sizeof(long long) * n;
+  void** bufs[] = {(void**)&kx, (void**)&ky, (void**)&kz, (void**)&kg, (void**)&ks};
+  for (void** b : bufs) RF_CUDA_TRY(v, cudaMallocAsync(b, bn, st));
+  for (int** b : {&ia, &ib, &flag, &seg, &inv}) RF_CUDA_TRY(v, cudaMallocAsync(b, sizeof(int) * n, st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&keep, sizeof(int) * std::max(m, 1), st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&pos, sizeof(int) * std::max(m, 1), st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&tr, sizeof(long long) * 3 * std::max(m, 1), st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&tmp, std::max({t_sort, t_scan, t_scan2}), st));
+  size_t tb = std::max({t_sort, t_scan, t_scan2});
+  k_weld_keys<<<g, 256, 0, st>>>(dv, n, tol, kx, ky, kz, ia);
+  // stable LSD: z, then y, then x -- lexicographic (x, y, z), ties by index
+  cub::DeviceRadixSort::SortPairs(tmp, tb, kz, ks, ia, ib, n, 0, 64, st);
+  k_weld_gather<<<g, 256, 0, st>>>(ky, ib, n, kg);
+  tb = std::max({t_sort, t_scan, t_scan2});
+  cub::DeviceRadixSort::SortPairs(tmp, tb, kg, ks, ib, ia, n, 0, 64, st);
+  k_weld_gather<<<g, 256, 0, st>>>(kx, ia, n, kg);
+  tb = std::max({t_sort, t_scan, t_scan2});
+  cub::DeviceRadixSort::SortPairs(tmp, tb, kg, ks, ia, ib, n, 0, 64, st);
+  k_weld_flags<<<g, 256, 0, st>>>(kx, ky, kz, ib, n, flag);
+  tb = std::max({t_sort, t_scan, t_scan2});
+  cub::DeviceScan::InclusiveSum(tmp, tb, flag, seg, n, st);
+  int nu = 0, nk = 0;
+  cudaMemcpyAsync(&nu, seg + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&vo, sizeof(double) * 3 * nu, st));
+  RF_CUDA_TRY(v, cudaMallocAsync(&co, sizeof(double) * 3 * nu, st));
+  k_weld_scatter<<<g, 256, 0, st>>>(ib, flag, seg, n, dv, dc, vo, co, inv);
+  if (m > 0) {
+    k_weld_tris<<<g, 256, 0, st>>>(dt, m, inv, tr, keep);
+    tb = std::max({t_sort, t_scan, t_scan2});
+    cub::DeviceScan::InclusiveSum(tmp, tb, keep, pos, m, st);
+    cudaMemcpyAsync(&nk, pos + (m - 1), sizeof(int), cudaMemcpyDeviceToHost, st);
+    RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  }
+  RF_CUDA_TRY(v, cudaMallocAsync(&to, sizeof(long long) * 3 * std::max(nk, 1), st));
+  if (m > 0) k_weld_compact<<<g, 256, 0, st>>>(tr, keep, pos, m, to);
+  for (void* p : {(void*)kx, (void*)ky, (void*)kz, (void*)kg, (void*)ks, (void*)ia, (void*)ib,
+                  (void*)flag, (void*)seg, (void*)inv, (void*)keep, (void*)pos, (void*)tr, tmp,
+                  (void*)dv, (void*)dc, (void*)dt})
+    cudaFreeAsync(p, st);
+  dv = vo;
+  dc = co;
+  dt = to;
+  nv = nu;
+  nt = nk;
+  return RF_OK;
+}
+
+// marching_cubes (+ optional device weld when tol > 0) into host arrays.
+rf_status mesh_to_host(rf_volume* v, double tol, double* vertices, double* colors,
+                       int64_t* triangles, int64_t vcap, int64_t tcap, int64_t* nv_out,
+                       int64_t* nt_out) {
   if (!v || !nv_out || !nt_out || vcap < 0 || tcap < 0) return RF_INVALID_ARG;
   cudaSetDevice(v->cfg.device);
   cudaStream_t st = v->stream;
@@ -1515,8 +1586,9 @@ rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int6
   if (cudaStreamSynchronize(st) != cudaSuccess) rs = RF_CUDA;
   *nv_out = tot[0];
   *nt_out = tot[1];
-  if (rs == RF_OK && vertices && colors && triangles && tot[0] <= vcap && tot[1] <= tcap &&
-      tot[0] > 0) {
+  const bool arrays = vertices && colors && triangles;
+  // unwelded sizes are known now; a welded mesh is sized by running the weld
+  if (rs == RF_OK && tot[0] > 0 && (tol > 0.0 || (arrays && tot[0] <= vcap && tot[1] <= tcap))) {
     double *dv = nullptr, *dc = nullptr;
     long long* dt = nullptr;
     if (cudaMallocAsync(&dv, sizeof(double) * 3 * tot[0], st) != cudaSuccess ||
@@ -1526,9 +1598,17 @@ rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int6
     } else {
       k_mesh_emit<<<grid, kMcThreads, 0, st>>>(v->T, keys_sorted, slots_sorted, n, off,
                                                off + (n + 1), v->cfg.voxel_size, dv, dc, dt);
-      cudaMemcpyAsync(vertices, dv, sizeof(double) * 3 * tot[0], cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(colors, dc, sizeof(double) * 3 * tot[0], cudaMemcpyDeviceToHost, st);
-      cudaMemcpyAsync(triangles, dt, sizeof(long long) * 3 * tot[1], cudaMemcpyDeviceToHost, st);
+      long long mv = tot[0], mt = tot[1];
+      if (tol > 0.0) {
+        rs = weld_device(v, tol, dv, dc, dt, mv, mt);
+        *nv_out = mv;
+        *nt_out = mt;
+      }
+      if (rs == RF_OK && arrays && mv <= vcap && mt <= tcap) {
+        cudaMemcpyAsync(vertices, dv, sizeof(double) * 3 * mv, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(colors, dc, sizeof(double) * 3 * mv, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(triangles, dt, sizeof(long long) * 3 * mt, cudaMemcpyDeviceToHost, st);
+      }
     }
     if (dv) cudaFreeAsync(dv, st);
     if (dc) cudaFreeAsync(dc, st);
@@ -1544,6 +1624,21 @@ rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int6
   return rs;
 }
 
+}  // namespace
+
+extern "C" {
+
+rf_status rf_marching_cubes(rf_volume* v, double* vertices, double* colors, int64_t* triangles,
+                            int64_t vcap, int64_t tcap, int64_t* nv_out, int64_t* nt_out) {
+  return mesh_to_host(v, 0.0, vertices, colors, triangles, vcap, tcap, nv_out, nt_out);
+}
+
+rf_status rf_marching_cubes_welded(rf_volume* v, double tol, double* vertices, double* colors,
+                                   int64_t* triangles, int64_t vcap, int64_t tcap,
+                                   int64_t* nv_out, int64_t* nt_out) {
+  if (!(tol > 0.0)) return RF_INVALID_ARG;
+  return mesh_to_host(v, tol, vertices, colors, triangles, vcap, tcap, nv_out, nt_out);
+}
 
 // ---- nn_min_d2 (_kernels_cy.pyx:111-129), the plugin's evaluation kernel ----
 

@@ -69,6 +69,26 @@ def marching_cubes(store, cfg):
     return TriangleMesh(vertices=v, colors=c, triangles=t[: nt.value])
 
 
+def welded_mesh(store, cfg, tol=1e-7):
+    """weld(marching_cubes(store, cfg), tol) with both steps on the device
+    (rf_marching_cubes_welded): only the welded mesh crosses to the host."""
+    if tol <= 0.0:
+        raise ValueError(f"tol must be > 0, got {tol}")
+    store._bind(cfg)
+    nv, nt = ctypes.c_int64(), ctypes.c_int64()
+    store._call("rf_marching_cubes_welded", float(tol), None, None, None, 0, 0,
+                ctypes.byref(nv), ctypes.byref(nt))
+    if nv.value == 0:
+        return TriangleMesh()
+    v = np.empty((nv.value, 3), dtype=np.float64)
+    c = np.empty((nv.value, 3), dtype=np.float64)
+    t = np.empty((max(nt.value, 1), 3), dtype=np.int64)
+    store._call("rf_marching_cubes_welded", float(tol), v.ctypes.data_as(L.c_double_p),
+                c.ctypes.data_as(L.c_double_p), t.ctypes.data_as(L.c_int64_p), nv.value,
+                nt.value, ctypes.byref(nv), ctypes.byref(nt))
+    return TriangleMesh(vertices=v, colors=c, triangles=t[: nt.value])
+
+
 def weld(mesh, tol=1e-7):
     """meshing.py:248-276 -- merge vertices on the same tol-grid point (the
     lowest index keeps its position and colour); drop triangles that collapse."""

@@ -139,6 +139,29 @@ def test_device_mc_matches_oracle_on_integrated_volume(V):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("name,seed,voxel", CASES)
+def test_device_weld_matches_reference_golden(V, name, seed, voxel):
+    from paper_1709_03763_b200 import meshing as M
+
+    keys, data, _ = S.mesh_volume(seed, voxel)
+    cfg = V.VolumeConfig(voxel_size=voxel, hash_buckets=1 << 12)
+    store = V.TwoTierStore(block_capacity=4096)
+    store._bind(cfg)
+    store._import(keys, data)
+    w = M.welded_mesh(store, cfg, 1e-7)
+    assert np.array_equal(w.vertices, GOLDEN[f"{name}_weld_vertices"])
+    assert np.array_equal(w.triangles, GOLDEN[f"{name}_weld_triangles"])
+    host = M.weld(M.marching_cubes(store, cfg), 1e-7)
+    assert np.array_equal(w.colors, host.colors)
+    # a coarse tolerance merges more (and collapses triangles): still numpy's result
+    coarse = M.welded_mesh(store, cfg, 2e-3)
+    want = M.weld(M.marching_cubes(store, cfg), 2e-3)
+    for a in ("vertices", "colors", "triangles"):
+        assert np.array_equal(getattr(coarse, a), getattr(want, a))
+    assert coarse.n_triangles < w.n_triangles
+
+
+@pytest.mark.gpu
 def test_device_mc_empty(V):
     from paper_1709_03763_b200 import meshing as M
 
@@ -146,8 +169,10 @@ def test_device_mc_empty(V):
     store = V.TwoTierStore(block_capacity=64)
     mesh = M.marching_cubes(store, cfg)
     assert mesh.n_vertices == 0 and mesh.n_triangles == 0
+    assert M.welded_mesh(store, cfg).n_vertices == 0
     store.put_block((0, 0, 0), d=np.ones(512), w=np.ones(512))  # no sign change
     assert M.marching_cubes(store, cfg).n_triangles == 0
+    assert M.welded_mesh(store, cfg).n_triangles == 0
 
 
 # ---------------------------------------------------------------------------

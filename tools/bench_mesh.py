@@ -63,6 +63,13 @@ def main():
         mesh = M.marching_cubes(store, cfg)
         t_full.append(time.perf_counter() - t0)
 
+    t_weld = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        welded = M.welded_mesh(store, cfg, 1e-7)
+        t_weld.append(time.perf_counter() - t0)
+
     # reference on a bounded sample of blocks (their +axis neighbours included)
     keys, d, w, c = store.export()
     rng = np.random.default_rng(0)
@@ -114,6 +121,8 @@ def main():
                          "blocks_per_s": round(1.0 / cpu_per_block, 1),
                          "extrapolated_s_whole_volume": round(cpu_per_block * n_blocks, 1)},
         "speedup_to_host": round(cpu_per_block * n_blocks / full, 1),
+        "welded_on_device_to_host_ms": round(1e3 * min(t_weld), 2),
+        "welded_vertices": welded.n_vertices, "welded_triangles": welded.n_triangles,
     }))
 
 
