@@ -21,6 +21,7 @@ is where the data lives:
 
 import ctypes
 import threading
+import weakref
 import os
 import struct
 from dataclasses import dataclass, field
@@ -199,7 +200,45 @@ def _host_plane(arr, shape):
     return a.ctypes.data, a
 
 
+_VIEWS = weakref.WeakKeyDictionary()  # keyframe -> (plane identities, device, view, keep)
+
+
 def kf_view(kf, device=0):
+    """kf_view_uncached, memoised per keyframe object while its plane objects
+    (and intrinsics) stay the same ones -- a correction re-marshals the same
+    keyframes every call.  In-place edits of a plane keep its pointer; the
+    footprint memo's content hash covers those."""
+    intr = kf.intrinsics
+    ident = (id(kf.depth), id(kf.weight), id(getattr(kf, "color", None)), id(intr), device)
+    try:
+        hit = _VIEWS.get(kf)
+    except TypeError:  # not weak-referenceable: no memo
+        return kf_view_uncached(kf, device)
+    if hit is not None and hit[0] == ident:
+        return hit[1], hit[2]
+    v, keep = kf_view_uncached(kf, device)
+    # memoise only views onto the keyframe's own memory (a converted or
+    # uploaded copy would go stale under an in-place edit of the plane)
+    own = [_own_ptr(kf.depth), _own_ptr(kf.weight)]
+    ptrs = [v.depth, v.weight]
+    if getattr(kf, "color", None) is not None:
+        own.append(_own_ptr(kf.color))
+        ptrs.append(v.color)
+    if all(o is not None and o == p for o, p in zip(own, ptrs)):
+        _VIEWS[kf] = (ident, v, keep)
+    return v, keep
+
+
+def _own_ptr(arr):
+    torch = _torch()
+    if isinstance(arr, torch.Tensor):
+        return arr.data_ptr()
+    if isinstance(arr, np.ndarray):
+        return arr.ctypes.data
+    return None
+
+
+def kf_view_uncached(kf, device=0):
     """(rf_kf_view, keep-alive objects) for a duck-typed keyframe.
 
     CUDA float64 planes on `device` are passed by pointer.  Planes in host
