@@ -106,10 +106,12 @@ struct rf_volume {
     double* buf = nullptr;
     size_t cap = 0;  // doubles
     cudaEvent_t ready = nullptr, consumed = nullptr;
+    cudaEvent_t color_ready = nullptr;  // colour plane uploaded (after depth + weight)
     const void* host = nullptr;  // host depth pointer staged in this batch
     bool used = false;
   };
   std::vector<StageSlot> stage;
+  std::unordered_map<const double*, cudaEvent_t> color_ready;  // staged colour plane -> upload event
   cudaStream_t copy_stream = nullptr;
   int stage_next = 0;
   int fp_grid_cap = 148 * 8;
@@ -578,14 +580,21 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
       if (!sl.ready) RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
       if (!sl.consumed)
         RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+      if (!sl.color_ready)
+        RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.color_ready, cudaEventDisableTiming));
       if (sl.used) cudaStreamWaitEvent(v->copy_stream, sl.consumed, 0);
+      // depth + weight first: the footprint and the removal check need only
+      // those, so they start while the colour plane is still in flight
       cudaMemcpyAsync(sl.buf, k.depth, sizeof(double) * npix, cudaMemcpyHostToDevice, v->copy_stream);
       cudaMemcpyAsync(sl.buf + npix, k.weight, sizeof(double) * npix, cudaMemcpyHostToDevice,
                       v->copy_stream);
-      if (k.color)
+      RF_CUDA_TRY(v, cudaEventRecord(sl.ready, v->copy_stream));
+      if (k.color) {
         cudaMemcpyAsync(sl.buf + 2 * npix, k.color, sizeof(double) * 3 * npix,
                         cudaMemcpyHostToDevice, v->copy_stream);
-      RF_CUDA_TRY(v, cudaEventRecord(sl.ready, v->copy_stream));
+        RF_CUDA_TRY(v, cudaEventRecord(sl.color_ready, v->copy_stream));
+        v->color_ready[sl.buf + 2 * npix] = sl.color_ready;
+      }
       sl.used = true;
       sl.host = k.depth;
       reuse = s;
@@ -609,6 +618,14 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
 void stage_consumed(rf_volume* v, const std::vector<int>& slot_of, int i) {
   if (i < static_cast<int>(slot_of.size()) && slot_of[i] >= 0)
     cudaEventRecord(v->stage[slot_of[i]].consumed, v->stream);
+}
+
+// A staged keyframe's colour plane may still be uploading: the kernels that
+// read colour (integrate / removal apply) wait for it.
+void wait_color(rf_volume* v, const rf_kf_view* kf) {
+  if (!kf->color || v->color_ready.empty()) return;
+  auto it = v->color_ready.find(kf->color);
+  if (it != v->color_ready.end()) cudaStreamWaitEvent(v->stream, it->second, 0);
 }
 
 // mode: 0 integrate, 1 deintegrate, 2 allocate only.  defer_removal (mode
@@ -675,6 +692,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
+  if (mode == 0) wait_color(v, kf);
   if (mode == 0 && merge) {
     {
       ProfScope ps(v, 0);
@@ -696,6 +714,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     }
     p.capture = nullptr;
     launches += 1;
+    wait_color(v, kf);  // the check read no colour; the removal does
     if (defer_removal && v->merge_pairs && !v->legacy_fuse && v->cfg.shard_count == 1) {
       b.pending_rm = op;
       b.pending_p = p;
@@ -974,6 +993,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
   for (auto& sl : v->stage) {
     if (sl.buf) cudaFree(sl.buf);
     if (sl.ready) cudaEventDestroy(sl.ready);
+    if (sl.color_ready) cudaEventDestroy(sl.color_ready);
     if (sl.consumed) cudaEventDestroy(sl.consumed);
   }
   if (v->copy_stream) cudaStreamDestroy(v->copy_stream);

@@ -11,6 +11,8 @@ the GPU), plus the drift / anchor-correction events of make_sequence
 import ctypes
 from dataclasses import dataclass
 
+import itertools
+
 import numpy as np
 
 from . import _lib as L
@@ -201,16 +203,25 @@ class Renderer:
         return depth, col
 
 
-class DeviceKeyframe:
-    """A keyframe whose planes live in HBM (duck-typed like Keyframe)."""
+_MEMO_TAGS = itertools.count(1)
 
-    def __init__(self, intrinsics, pose, depth, weight, color, kf_id=-1):
+
+class DeviceKeyframe:
+    """A keyframe whose planes live in HBM (duck-typed like Keyframe).
+
+    ``memo_tag`` identifies the keyframe to the volume's footprint memo
+    (rf_kf_view.memo_tag): its host copy (to_host) keeps the tag, so a
+    de-integration from host planes reuses the footprint its resident twin
+    integrated (the memo still checks the planes' content hash)."""
+
+    def __init__(self, intrinsics, pose, depth, weight, color, kf_id=-1, memo_tag=None):
         self.intrinsics = intrinsics
         self.pose = pose
         self.depth = depth
         self.weight = weight
         self.color = color
         self.kf_id = kf_id
+        self.memo_tag = next(_MEMO_TAGS) if memo_tag is None else memo_tag
 
     def to_host(self, pinned=False):
         """Host copy with the same attributes (numpy, or pinned torch tensors)."""
@@ -220,7 +231,8 @@ class DeviceKeyframe:
         else:
             planes = [None if t is None else t.cpu().numpy()
                       for t in (self.depth, self.weight, self.color)]
-        return DeviceKeyframe(self.intrinsics, self.pose, *planes, kf_id=self.kf_id)
+        return DeviceKeyframe(self.intrinsics, self.pose, *planes, kf_id=self.kf_id,
+                              memo_tag=self.memo_tag)
 
 
 def render_keyframe(renderer, pose, seed, kappa=5):

@@ -268,6 +268,7 @@ def kf_view_uncached(kf, device=0):
         ptrs = [t.data_ptr() for t in keep]
     v.depth, v.weight = ptrs[0], ptrs[1]
     v.color = ptrs[2] if color is not None else None
+    v.memo_tag = int(getattr(kf, "memo_tag", 0) or 0) & 0xFFFFFFFFFFFFFFFF
     return v, keep
 
 
