@@ -21,6 +21,9 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "refusion_b200.h"
@@ -331,6 +334,58 @@ __global__ void k_blur_lines(const double* __restrict__ f, int W, int H, int axi
   }
 }
 
+// The same per line, one warp per line through shared memory: the lanes load
+// the line (coalesced along rows), lane 0 runs the sequential running sum out
+// of shared memory (scipy's order, so the bits match k_blur_lines), and the
+// lanes then write the filtered line and its diffs in parallel.
+constexpr int kBlurWarps = 4;
+constexpr int kBlurMaxLen = 3072;  // 2 x 8 B x len per warp in dynamic smem
+
+__global__ void __launch_bounds__(32 * kBlurWarps)
+    k_blur_lines_smem(const double* __restrict__ f, int W, int H, int axis, int size,
+                      double* __restrict__ b, double* __restrict__ d_f,
+                      double* __restrict__ vv) {
+  extern __shared__ double s_blur[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int line = blockIdx.x * kBlurWarps + warp;
+  const int lines = axis == 0 ? W : H;
+  if (line >= lines) return;
+  const int len = axis == 0 ? H : W;
+  const size_t stride = axis == 0 ? W : 1;
+  const double* src = f + (axis == 0 ? line : static_cast<size_t>(line) * W);
+  double* dst = b + (axis == 0 ? line : static_cast<size_t>(line) * W);
+  double* s_in = s_blur + static_cast<size_t>(warp) * 2 * len;
+  double* s_out = s_in + len;
+  for (int k = lane; k < len; k += 32) s_in[k] = src[static_cast<size_t>(k) * stride];
+  __syncwarp();
+  if (lane == 0) {  // the running sums (sequential); the lanes divide below
+    const int s1 = size / 2;
+    auto at = [&](int k) { return s_in[min(max(k, 0), len - 1)]; };
+    double tmp = 0.0;
+    for (int l = 0; l < size; ++l) tmp = tmp + at(l - s1);
+    s_out[0] = tmp;
+#pragma unroll 8
+    for (int l = 1; l < len; ++l) {
+      tmp = tmp + (at(l + size - 1 - s1) - at(l - 1 - s1));
+      s_out[l] = tmp;
+    }
+  }
+  __syncwarp();
+  for (int l = lane; l < len; l += 32) s_out[l] = s_out[l] / size;
+  __syncwarp();
+  for (int l = lane; l < len; l += 32) {
+    dst[static_cast<size_t>(l) * stride] = s_out[l];
+    if (l + 1 < len) {
+      const double df = fabs(s_in[l + 1] - s_in[l]);
+      const double db = fabs(s_out[l + 1] - s_out[l]);
+      const size_t o = axis == 0 ? static_cast<size_t>(l) * W + line
+                                 : static_cast<size_t>(line) * (W - 1) + l;
+      d_f[o] = df;
+      vv[o] = fmax(0.0, df - db);
+    }
+  }
+}
+
 // numpy pairwise summation (pairwise_sum in loops_utils.h): blocks of <=128
 // elements with 8 accumulators, recursive halving at multiples of 8.
 __device__ double pairwise_leaf(const double* a, long long n) {
@@ -357,18 +412,22 @@ struct PwNode {
   double val;
 };
 
-__global__ void k_pairwise_leaves(const double* a, PwNode* nodes, int n_nodes) {
+// Leaves of the pairwise tree (numpy's blocks of <= 128), all in parallel.
+__global__ void k_pairwise_leaves(const double* a, const PwNode* nodes, int n_leaves, double* val) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k >= n_nodes || nodes[k].left >= 0) return;
-  nodes[k].val = pairwise_leaf(a + nodes[k].off, nodes[k].n);
+  if (k < n_leaves) val[k] = pairwise_leaf(a + nodes[k].off, nodes[k].n);
 }
 
-__global__ void k_pairwise_combine(PwNode* nodes, int n_nodes, double* out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  // nodes are stored so that children precede parents (post-order)
-  for (int k = 0; k < n_nodes; ++k)
-    if (nodes[k].left >= 0) nodes[k].val = nodes[nodes[k].left].val + nodes[nodes[k].right].val;
-  *out = nodes[n_nodes - 1].val;
+// Internal nodes level by level (nodes sorted by height, children first):
+// one CTA, a barrier per level -- the additions are numpy's, in its order.
+__global__ void __launch_bounds__(1024) k_pairwise_levels(const PwNode* nodes, const int* level_off,
+                                                          int n_levels, double* val, double* out) {
+  for (int l = 1; l < n_levels; ++l) {
+    for (int k = level_off[l] + threadIdx.x; k < level_off[l + 1]; k += blockDim.x)
+      val[k] = val[nodes[k].left] + val[nodes[k].right];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = val[level_off[n_levels] - 1];
 }
 
 // blurriness (:310-332): scores (s_f - v.sum()) / s_f per axis with s_f > 0
@@ -404,6 +463,12 @@ struct MemberDev {
   rf_pose rel;
 };
 
+// The member table travels as a kernel parameter (8 KB; no host->device
+// copy that would wait for the stream).
+struct MemberTable {
+  MemberDev m[kMaxMembers];
+};
+
 __device__ __forceinline__ void bilinear(const double* img, int W, int H, double u, double v,
                                          double out[3]) {  // _bilinear (:362-374)
   long long u0 = static_cast<long long>(floor(u)), v0 = static_cast<long long>(floor(v));
@@ -422,7 +487,7 @@ __device__ __forceinline__ void bilinear(const double* img, int W, int H, double
 }
 
 __global__ void k_fuse_color(const double* __restrict__ kd, const double* __restrict__ kw, Intr in,
-                             const MemberDev* __restrict__ mem, int n_mem, double delta_occl,
+                             const __grid_constant__ MemberTable tab, int n_mem, double delta_occl,
                              int order, double* __restrict__ color_out,
                              unsigned char* __restrict__ valid_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -440,7 +505,7 @@ __global__ void k_fuse_color(const double* __restrict__ kd, const double* __rest
   for (int m = 0; m < n_mem; ++m) {
     vals[m][0] = vals[m][1] = vals[m][2] = 0.0;
     wts[m] = 0.0;
-    const MemberDev& M = mem[m];
+    const MemberDev& M = tab.m[m];
     double q0, q1, q2;
     transform(M.rel, p0, p1, z, order, q0, q1, q2);
     if (!(q2 > 0)) continue;
@@ -510,17 +575,150 @@ int build_pairwise_tree(long long off, long long n, std::vector<PwNode>& out) {
   return static_cast<int>(out.size()) - 1;
 }
 
-rf_status pairwise_sum(const double* a, long long n, double* out, cudaStream_t s) {
-  std::vector<PwNode> nodes;
-  build_pairwise_tree(0, n, nodes);
-  PwNode* d = nullptr;
-  if (cudaMallocAsync(&d, sizeof(PwNode) * nodes.size(), s) != cudaSuccess) return RF_CUDA;
-  cudaMemcpyAsync(d, nodes.data(), sizeof(PwNode) * nodes.size(), cudaMemcpyHostToDevice, s);
-  const int nn = static_cast<int>(nodes.size());
-  k_pairwise_leaves<<<(nn + 127) / 128, 128, 0, s>>>(a, d, nn);
-  k_pairwise_combine<<<1, 1, 0, s>>>(d, nn, out);
-  cudaFreeAsync(d, s);
+// numpy's pairwise tree for n elements, sorted by height and uploaded once
+// per (device, n): [leaves | height-1 nodes | ...], children before parents.
+struct PwTree {
+  PwNode* nodes = nullptr;
+  int* level_off = nullptr;
+  int n_nodes = 0, n_leaves = 0, n_levels = 0;
+};
+
+const PwTree* pairwise_tree(long long n) {
+  static std::map<std::pair<int, long long>, PwTree> cache;
+  static std::mutex mu;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, n});
+  if (it != cache.end()) return &it->second;
+  std::vector<PwNode> post;
+  build_pairwise_tree(0, n, post);
+  const int m = static_cast<int>(post.size());
+  std::vector<int> height(m, 0);
+  int max_h = 0;
+  for (int k = 0; k < m; ++k)  // post-order: children first
+    if (post[k].left >= 0) {
+      height[k] = std::max(height[post[k].left], height[post[k].right]) + 1;
+      max_h = std::max(max_h, height[k]);
+    }
+  std::vector<int> order(m), pos(m), level_off(max_h + 2, 0);
+  for (int k = 0; k < m; ++k) ++level_off[height[k] + 1];
+  for (int h = 0; h <= max_h; ++h) level_off[h + 1] += level_off[h];
+  std::vector<int> fill(level_off.begin(), level_off.end() - 1);
+  for (int k = 0; k < m; ++k) pos[k] = fill[height[k]]++;  // stable within a level
+  std::vector<PwNode> sorted(m);
+  for (int k = 0; k < m; ++k) {
+    PwNode e = post[k];
+    if (e.left >= 0) {
+      e.left = pos[e.left];
+      e.right = pos[e.right];
+    }
+    sorted[pos[k]] = e;
+  }
+  PwTree t;
+  t.n_nodes = m;
+  t.n_leaves = level_off[1];
+  t.n_levels = max_h + 1;
+  if (cudaMalloc(&t.nodes, sizeof(PwNode) * m) != cudaSuccess ||
+      cudaMalloc(&t.level_off, sizeof(int) * level_off.size()) != cudaSuccess)
+    return nullptr;
+  cudaMemcpy(t.nodes, sorted.data(), sizeof(PwNode) * m, cudaMemcpyHostToDevice);
+  cudaMemcpy(t.level_off, level_off.data(), sizeof(int) * level_off.size(), cudaMemcpyHostToDevice);
+  return &cache.emplace(std::make_pair(dev, n), t).first->second;
+}
+
+// Up to four pairwise sums at once: leaves of all trees in one grid, then
+// one CTA per tree for the levels.
+struct PwBatch {
+  const double* a[4];
+  const PwNode* nodes[4];
+  const int* level_off[4];
+  double* val[4];
+  double* out[4];
+  int n_leaves[4], n_levels[4], leaf_base[5];
+};
+
+__global__ void k_pairwise_leaves_batch(PwBatch b) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  int t = 0;
+  while (t < 3 && k >= b.leaf_base[t + 1]) ++t;
+  const int j = k - b.leaf_base[t];
+  if (k >= b.leaf_base[4] || j >= b.n_leaves[t]) return;
+  b.val[t][j] = pairwise_leaf(b.a[t] + b.nodes[t][j].off, b.nodes[t][j].n);
+}
+
+__global__ void __launch_bounds__(1024) k_pairwise_levels_batch(PwBatch b) {
+  const int t = blockIdx.x;
+  const PwNode* nodes = b.nodes[t];
+  const int* lo = b.level_off[t];
+  double* val = b.val[t];
+  for (int l = 1; l < b.n_levels[t]; ++l) {
+    for (int k = lo[l] + threadIdx.x; k < lo[l + 1]; k += blockDim.x)
+      val[k] = val[nodes[k].left] + val[nodes[k].right];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *b.out[t] = val[lo[b.n_levels[t]] - 1];
+}
+
+rf_status pairwise_sums(int count, const double* const* a, const long long* n, double* const* out,
+                        cudaStream_t s) {
+  PwBatch b{};
+  double* val = nullptr;
+  long long total_nodes = 0;
+  const PwTree* trees[4];
+  for (int t = 0; t < count; ++t) {
+    trees[t] = pairwise_tree(n[t]);
+    if (!trees[t]) return RF_CUDA;
+    total_nodes += trees[t]->n_nodes;
+  }
+  if (cudaMallocAsync(&val, sizeof(double) * total_nodes, s) != cudaSuccess) return RF_CUDA;
+  long long vo = 0;
+  b.leaf_base[0] = 0;
+  for (int t = 0; t < 4; ++t) {
+    const bool on = t < count;
+    b.a[t] = on ? a[t] : nullptr;
+    b.nodes[t] = on ? trees[t]->nodes : nullptr;
+    b.level_off[t] = on ? trees[t]->level_off : nullptr;
+    b.val[t] = on ? val + vo : nullptr;
+    b.out[t] = on ? out[t] : nullptr;
+    b.n_leaves[t] = on ? trees[t]->n_leaves : 0;
+    b.n_levels[t] = on ? trees[t]->n_levels : 0;
+    b.leaf_base[t + 1] = b.leaf_base[t] + b.n_leaves[t];
+    if (on) vo += trees[t]->n_nodes;
+  }
+  k_pairwise_leaves_batch<<<(b.leaf_base[4] + 127) / 128, 128, 0, s>>>(b);
+  k_pairwise_levels_batch<<<count, 1024, 0, s>>>(b);
+  cudaFreeAsync(val, s);
   return RF_OK;
+}
+
+rf_status pairwise_sum(const double* a, long long n, double* out, cudaStream_t s) {
+  const PwTree* t = pairwise_tree(n);
+  if (!t) return RF_CUDA;
+  double* val = nullptr;
+  if (cudaMallocAsync(&val, sizeof(double) * t->n_nodes, s) != cudaSuccess) return RF_CUDA;
+  k_pairwise_leaves<<<(t->n_leaves + 127) / 128, 128, 0, s>>>(a, t->nodes, t->n_leaves, val);
+  k_pairwise_levels<<<1, 1024, 0, s>>>(t->nodes, t->level_off, t->n_levels, val, out);
+  cudaFreeAsync(val, s);
+  return RF_OK;
+}
+
+// The stream-ordered pool keeps what it allocated between calls (the fusion
+// entry points allocate scratch per call; releasing it at every host sync
+// would re-map device memory on the next call).
+void keep_pool() {
+  static std::mutex mu;
+  static std::vector<int> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(done.begin(), done.end(), dev) != done.end()) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    unsigned long long thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.push_back(dev);
 }
 
 }  // namespace
@@ -544,6 +742,7 @@ rf_status rf_fuse_depth(double* kf_depth, double* kf_weight, const double* frame
                         void* stream) {
   if (!kf_depth || !kf_weight || !frame_depth || !w_map || !rel || width <= 0 || height <= 0)
     return RF_INVALID_ARG;
+  keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = width * height;
   const int nb = (n + kScanBlock - 1) / kScanBlock;
@@ -583,6 +782,7 @@ rf_status rf_unsharp_mask(const double* img, int32_t width, int32_t height, int3
   if (!img || !out || !gauss_weights || width <= 0 || height <= 0 || channels <= 0 ||
       radius < 0 || radius > 15)
     return RF_INVALID_ARG;
+  keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long n = static_cast<long long>(width) * height * channels;
   if (gain == 0.0) {  // unsharp_mask returns img.copy() (:338-339)
@@ -612,32 +812,52 @@ rf_status rf_grayscale(const double* color, int32_t width, int32_t height, doubl
 rf_status rf_blurriness(const double* gray, int32_t width, int32_t height, double* blur_weight,
                         void* stream) {
   if (!gray || !blur_weight || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long n = static_cast<long long>(width) * height;
-  double *b = nullptr, *d_f = nullptr, *vv = nullptr, *sums = nullptr;
+  double *b = nullptr, *buf = nullptr, *sums = nullptr;
   bool ok = cudaMallocAsync(&b, sizeof(double) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&d_f, sizeof(double) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&vv, sizeof(double) * n, s) == cudaSuccess &&
+            cudaMallocAsync(&buf, sizeof(double) * 4 * n, s) == cudaSuccess &&
             cudaMallocAsync(&sums, sizeof(double) * 4, s) == cudaSuccess;
   rf_status st = ok ? RF_OK : RF_CUDA;
   if (ok) {
+    // per axis: d_f and v = max(0, d_f - d_b), then the four pairwise sums at once
+    const double* arr[4];
+    long long cnt[4];
+    double* outs[4];
     int axes = 0;
-    double* sum_ptr = sums;
     for (int axis = 0; axis < 2; ++axis) {
       const int len = axis == 0 ? height : width;
       if (len < 2) continue;
       const int lines = axis == 0 ? width : height;
-      k_blur_lines<<<(lines + 63) / 64, 64, 0, s>>>(gray, width, height, axis, 9, b, d_f, vv);
+      double* d_f = buf + 2 * axes * n;
+      double* vv = d_f + n;
+      if (len <= kBlurMaxLen) {
+        static bool attr = false;
+        if (!attr) {
+          cudaFuncSetAttribute(k_blur_lines_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sizeof(double) * 2 * kBlurMaxLen * kBlurWarps));
+          attr = true;
+        }
+        k_blur_lines_smem<<<(lines + kBlurWarps - 1) / kBlurWarps, 32 * kBlurWarps,
+                            sizeof(double) * 2 * len * kBlurWarps, s>>>(gray, width, height, axis,
+                                                                       9, b, d_f, vv);
+      } else {
+        k_blur_lines<<<(lines + 63) / 64, 64, 0, s>>>(gray, width, height, axis, 9, b, d_f, vv);
+      }
       const long long m = axis == 0 ? static_cast<long long>(height - 1) * width
                                     : static_cast<long long>(height) * (width - 1);
-      if (pairwise_sum(d_f, m, sum_ptr, s) != RF_OK || pairwise_sum(vv, m, sum_ptr + 1, s) != RF_OK)
-        st = RF_CUDA;
-      sum_ptr += 2;
+      arr[2 * axes] = d_f;
+      arr[2 * axes + 1] = vv;
+      cnt[2 * axes] = cnt[2 * axes + 1] = m;
+      outs[2 * axes] = sums + 2 * axes;
+      outs[2 * axes + 1] = sums + 2 * axes + 1;
       ++axes;
     }
+    if (axes > 0 && pairwise_sums(2 * axes, arr, cnt, outs, s) != RF_OK) st = RF_CUDA;
     k_blur_finish<<<1, 1, 0, s>>>(sums, axes, blur_weight);
   }
-  void* bufs[] = {b, d_f, vv, sums};
+  void* bufs[] = {b, buf, sums};
   for (void* p : bufs)
     if (p) cudaFreeAsync(p, s);
   if (st != RF_OK) return st;
@@ -648,6 +868,7 @@ rf_status rf_color_prep(const double* color, int32_t width, int32_t height,
                         const double* gauss_weights, int32_t radius, double gain,
                         double* member_color, double* blur_weight, void* stream) {
   if (!color || !member_color || !blur_weight) return RF_INVALID_ARG;
+  keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   double* gray = nullptr;
   if (cudaMallocAsync(&gray, sizeof(double) * width * height, s) != cudaSuccess) return RF_CUDA;
@@ -667,6 +888,7 @@ rf_status rf_fuse_color(const double* kf_depth, const double* kf_weight, int32_t
   if (!kf_depth || !kf_weight || !kf_color || !color_valid || width <= 0 || height <= 0 ||
       n_members < 0 || n_members > kMaxMembers || (n_members > 0 && !members))
     return RF_INVALID_ARG;
+  keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   std::vector<MemberDev> host(static_cast<size_t>(std::max(n_members, 1)));
   for (int m = 0; m < n_members; ++m) {
@@ -678,15 +900,13 @@ rf_status rf_fuse_color(const double* kf_depth, const double* kf_weight, int32_t
     host[m].blur = members[m].blur_weight;
     host[m].rel = members[m].rel;
   }
-  MemberDev* d = nullptr;
-  if (cudaMallocAsync(&d, sizeof(MemberDev) * host.size(), s) != cudaSuccess) return RF_CUDA;
-  cudaMemcpyAsync(d, host.data(), sizeof(MemberDev) * host.size(), cudaMemcpyHostToDevice, s);
+  MemberTable tab{};
+  for (int m = 0; m < n_members; ++m) tab.m[m] = host[m];
   const int n = width * height;
   k_fuse_color<<<(n + 127) / 128, 128, 0, s>>>(kf_depth, kf_weight,
-                                                make_intr(width, height, fx, fy, cx, cy), d,
+                                                make_intr(width, height, fx, fy, cx, cy), tab,
                                                 n_members, delta_occl, blas_order, kf_color,
                                                 color_valid);
-  cudaFreeAsync(d, s);
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }
 
