@@ -216,6 +216,13 @@ rf_status rf_marching_cubes_welded(rf_volume *vol, double tol, double *vertices,
  * NULL.  Needs no volume. */
 rf_status rf_nn_min_d2(const double *q, int64_t n, const double *pts, int64_t m, double *out,
                        void *stream);
+/* save_volume's SDFV1 records (volume.py:397-415), streamed: records_host
+ * receives blocks [first, first + count) in sorted coordinate order, each
+ * 3 x int32 coordinate + 512 x 5 f64 (D, W, C0, C1, C2 per voxel) = 20,492 B,
+ * byte-identical to the reference's file body; *total = block count
+ * (records_host may be NULL to query it). */
+rf_status rf_snapshot_records(rf_volume *vol, int64_t first, int64_t count, void *records_host,
+                              int64_t *total);
 /* insert blocks with the given contents (load_volume, volume.py:418-442) */
 rf_status rf_import_blocks(rf_volume *vol, const int64_t *keys_host,
                            const double *data_host, int64_t n);

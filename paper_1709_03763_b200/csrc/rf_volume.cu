@@ -1443,6 +1443,55 @@ rf_status rf_counters_get(rf_volume* v, rf_counters* out) {
   return RF_OK;
 }
 
+// save_volume's records, streamed: blocks in sorted coordinate order
+// (volume.py:399-401), [first, first + count) of them per call.
+rf_status rf_snapshot_records(rf_volume* v, int64_t first, int64_t count, void* records_host,
+                              int64_t* total) {
+  if (!v || !total || first < 0 || count < 0) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaStream_t st = v->stream;
+  int* d_list = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_list, sizeof(int) * v->T.capacity, st));
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), st);
+  k_list_live<<<v->n_sms * 4, 256, 0, st>>>(v->T, d_list, v->d_u64);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  const long long n = static_cast<long long>(v->h_u64[0]);
+  *total = n;
+  const long long m = std::max(0LL, std::min<long long>(count, n - first));
+  rf_status rs = RF_OK;
+  if (records_host && m > 0) {
+    long long *keys = nullptr, *keys_sorted = nullptr;
+    int* slots_sorted = nullptr;
+    unsigned* rec = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, (long long*)nullptr, (long long*)nullptr,
+                                    (int*)nullptr, (int*)nullptr, static_cast<int>(n), 0, 63, st);
+    if (cudaMallocAsync(&keys, sizeof(long long) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&keys_sorted, sizeof(long long) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&slots_sorted, sizeof(int) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&tmp, tmp_bytes, st) != cudaSuccess ||
+        cudaMallocAsync(&rec, sizeof(unsigned) * kSnapRecordWords * m, st) != cudaSuccess) {
+      rs = RF_CAPACITY;
+    } else {
+      k_gather_keys<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(v->T, d_list, n, keys);
+      cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_sorted, d_list, slots_sorted,
+                                      static_cast<int>(n), 0, 63, st);
+      k_snapshot_records<<<static_cast<int>(std::min<long long>(m, v->n_sms * 16)), 256, 0, st>>>(
+          v->T, slots_sorted, first, m, rec);
+      cudaMemcpyAsync(records_host, rec, sizeof(unsigned) * kSnapRecordWords * m,
+                      cudaMemcpyDeviceToHost, st);
+    }
+    for (void* p : {(void*)keys, (void*)keys_sorted, (void*)slots_sorted, (void*)rec, tmp})
+      if (p) cudaFreeAsync(p, st);
+  }
+  cudaFreeAsync(d_list, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return fail(v, RF_CUDA, "snapshot records failed");
+  if (rs != RF_OK) return fail(v, rs, "snapshot records: device memory");
+  return RF_OK;
+}
+
 rf_status rf_export_blocks(rf_volume* v, int64_t* keys_host, double* data_host, int64_t cap,
                            int64_t* n_out) {
   if (!v || !n_out) return RF_INVALID_ARG;

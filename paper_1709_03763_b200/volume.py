@@ -802,19 +802,42 @@ def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640
 _MAGIC = b"SDFV1"
 
 
+_RECORD = np.dtype([("coord", "<i4", (3,)), ("rec", "<f8", (BLOCK_VOXELS, 5))])  # 20,492 B
+_SNAP_CHUNK = 8192  # blocks per device -> host chunk (168 MB)
+
+
 def save_volume(store, path, cfg):
-    keys, d, w, c = store.export()
-    coords = unpack_keys(keys)
+    """volume.py:397-415 -- the SDFV1 snapshot, byte for byte: the records are
+    formatted on the device in sorted coordinate order and streamed to the
+    file in chunks (the volume never sits in host memory whole)."""
+    if not store.bound:  # blocks loaded but never bound: write them from the host
+        keys, d, w, c = store.export()
+        order = np.argsort(keys, kind="stable")
+        recs = np.empty(len(keys), dtype=_RECORD)
+        recs["coord"] = unpack_keys(keys[order])
+        recs["rec"][:, :, 0] = d[order]
+        recs["rec"][:, :, 1] = w[order]
+        recs["rec"][:, :, 2:] = c[order]
+        with open(path, "wb") as fh:
+            fh.write(_MAGIC)
+            fh.write(struct.pack("<ddq", cfg.voxel_size, cfg.mu, len(keys)))
+            fh.write(recs.tobytes())
+        return
+    store._bind(cfg)
+    total = ctypes.c_int64()
+    store._call("rf_snapshot_records", 0, 0, None, ctypes.byref(total))
+    n = int(total.value)
+    buf = np.empty(min(n, _SNAP_CHUNK), dtype=_RECORD)
     with open(path, "wb") as fh:
         fh.write(_MAGIC)
-        fh.write(struct.pack("<ddq", cfg.voxel_size, cfg.mu, len(keys)))
-        for i in range(len(keys)):
-            fh.write(struct.pack("<iii", *(int(x) for x in coords[i])))
-            rec = np.empty((BLOCK_VOXELS, 5))
-            rec[:, 0] = d[i]
-            rec[:, 1] = w[i]
-            rec[:, 2:] = c[i]
-            fh.write(rec.astype("<f8").tobytes())
+        fh.write(struct.pack("<ddq", cfg.voxel_size, cfg.mu, n))
+        for first in range(0, n, _SNAP_CHUNK):
+            m = min(_SNAP_CHUNK, n - first)
+            store._call("rf_snapshot_records", first, m, buf.ctypes.data_as(ctypes.c_void_p),
+                        ctypes.byref(total))
+            if int(total.value) != n:
+                raise RuntimeError("volume changed while it was being saved")
+            fh.write(memoryview(buf[:m]).cast("B"))
 
 
 def load_volume(path, block_capacity=None, device=None):
@@ -825,16 +848,14 @@ def load_volume(path, block_capacity=None, device=None):
         if magic != _MAGIC:
             raise ValueError(f"not a volume snapshot: bad magic {magic!r}")
         voxel_size, mu, count = struct.unpack("<ddq", fh.read(24))
-        coords = np.zeros((count, 3), dtype=np.int64)
-        data = np.zeros((count, 5, BLOCK_VOXELS))
-        for i in range(count):
-            coords[i] = struct.unpack("<iii", fh.read(12))
-            rec = np.frombuffer(fh.read(BLOCK_VOXELS * 5 * 8), dtype="<f8").reshape(BLOCK_VOXELS, 5)
-            data[i] = rec.T
+        recs = np.fromfile(fh, dtype=_RECORD, count=count)
+    if len(recs) != count:
+        raise ValueError(f"truncated snapshot: {len(recs)} of {count} blocks")
     store = TwoTierStore(block_capacity=block_capacity or max(count, DEFAULT_BLOCK_CAPACITY),
                          device=device)
     if count:
-        store._pending = (pack_keys(coords), data)
+        data = np.ascontiguousarray(np.transpose(recs["rec"], (0, 2, 1)))
+        store._pending = (pack_keys(recs["coord"].astype(np.int64)), data)
     return store, voxel_size, mu
 
 

@@ -270,6 +270,44 @@ def test_save_load_roundtrip(V, tmp_path):
     assert V.compare_volumes(store, loaded) == (0.0, 0.0, 0.0)
 
 
+def test_snapshot_bytes_match_reference(V, tmp_path):
+    """save_volume streams SDFV1 records formatted on the device: the file is
+    byte-identical to the reference's save_volume of the same blocks, and the
+    reference's file loads back bit for bit (volume.py:397-442)."""
+    from refimport import reference
+
+    ref = reference()
+    if ref is None:
+        pytest.skip("reference build (oracle/_ref) absent")
+    RV = ref["V"]
+    rng = np.random.default_rng(71)
+    cfg = V.VolumeConfig(voxel_size=0.01, mu=0.06, stream_radius=4.0)
+    pose = S.SPose(S.rot_y(0.15), [0.05, 0.0, 0.1])
+    store = V.TwoTierStore(block_capacity=1 << 12)
+    V.stream(store, pose.translation, cfg)
+    for _ in range(2):
+        V.integrate(store, S.random_frame(rng), pose, cfg)
+    old_chunk = V._SNAP_CHUNK
+    V._SNAP_CHUNK = 7  # several chunks
+    try:
+        ours = tmp_path / "ours.sdf"
+        V.save_volume(store, os.fspath(ours), cfg)
+    finally:
+        V._SNAP_CHUNK = old_chunk
+    keys, d, w, c = store.export()
+    rs = RV.TwoTierStore()
+    for k, dd, ww, cc in zip(keys, d, w, c):
+        coord = tuple(int(x) for x in V.unpack_keys(np.array([k]))[0])
+        rs.active[coord] = RV.VoxelBlock(coord, dd.copy(), ww.copy(), cc.copy())
+    theirs = tmp_path / "ref.sdf"
+    RV.save_volume(rs, os.fspath(theirs), RV.VolumeConfig(voxel_size=cfg.voxel_size, mu=cfg.mu))
+    assert ours.read_bytes() == theirs.read_bytes()
+    loaded, vs, mu = V.load_volume(os.fspath(theirs))
+    V.stream(loaded, np.zeros(3), cfg)
+    for a, b in zip(loaded.export(), store.export()):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("exp_span", [8, 60, 600])
 def test_shared_denominator_division_is_ieee(exp_span):
     """The kernels divide by Markstein correction with a shared reciprocal;
