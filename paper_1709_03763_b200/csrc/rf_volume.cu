@@ -908,13 +908,6 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
     g_pdl = !(pdl && std::string(pdl) == "0");
     const char* mp = std::getenv("RF_MERGE_PAIRS");
     v->merge_pairs = mp && std::string(mp) == "1";
-    const char* gran = std::getenv("RF_L2_FETCH");
-    if (gran) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, std::strtoul(gran, nullptr, 10));
-    if (std::getenv("RF_VERBOSE")) {
-      size_t g = 0;
-      cudaDeviceGetLimit(&g, cudaLimitMaxL2FetchGranularity);
-      std::fprintf(stderr, "rf: L2 fetch granularity %zu B\n", g);
-    }
   }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
