@@ -178,9 +178,12 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (RF_DIST_BACKEND=gloo with fewer GPUs than ranks: a functional check of
+    # the multi-rank path with ranks sharing devices -- not a measurement)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
+        dist.init_process_group(os.environ.get("RF_DIST_BACKEND", "nccl"))
     dev = torch.device(f"cuda:{local}")
 
     n_kf = args.keyframes
