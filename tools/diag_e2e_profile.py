@@ -1,0 +1,95 @@
+"""Where the end-to-end correction time goes: the bench's corrections with
+keyframes resident vs uploaded from pinned host memory, each with the wall
+time, the device-event time around the call, and rf_profile's per-kernel-class
+device time (fuse / check / footprint / other).  Diagnostic only."""
+
+import ctypes
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import bench as B  # noqa: E402
+
+
+def main():
+    import torch
+
+    from paper_1709_03763_b200 import _lib as L
+    from paper_1709_03763_b200 import geometry as G
+    from paper_1709_03763_b200 import reintegration as R
+    from paper_1709_03763_b200 import synth as SY
+    from paper_1709_03763_b200 import volume as V
+
+    torch.cuda.set_device(0)
+    n_kf = int(os.environ.get("KF", "200"))
+    steps = 8
+    gt, dr = B.kf_poses(n_kf)
+    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=0)
+    kfs = []
+    for k in range(n_kf):
+        kf = SY.render_keyframe(rend, gt[k], seed=1000 + k, kappa=B.KAPPA)
+        kf.pose = dr[k]
+        kfs.append(kf)
+    cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
+                         hash_buckets=1 << 21)
+    store = V.TwoTierStore(block_capacity=2_000_000)
+    for kf, p in zip(kfs, dr):
+        V.stream(store, p.translation, cfg)
+        V.integrate(store, kf, p, cfg)
+    torch.cuda.synchronize()
+    n_anchors = (n_kf + B.EVENT_EVERY_KF - 1) // B.EVENT_EVERY_KF
+    events = B.make_events(n_anchors, 4 * steps + 8)
+    scen = B.Scenario(R, G, SY, gt, dr, kfs, events)
+    lib = L.lib()
+    stream = torch.cuda.current_stream()
+    idx = [0]
+
+    def one():
+        ev = scen.event(idx[0])
+        idx[0] += 1
+        R.apply_pose_update(scen.ledger, ev)
+        picks = R.select_topk(scen.ledger, B.M_TOPK)
+        nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        t = time.perf_counter()
+        a.record(stream)
+        R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+        b.record(stream)
+        b.synchronize()
+        return 1e3 * (time.perf_counter() - t), a.elapsed_time(b)
+
+    def phase(label):
+        for _ in range(3):
+            one()
+        lib.rf_profile_begin(store._ptr)
+        walls, devs = [], []
+        for _ in range(steps):
+            w, d = one()
+            walls.append(w)
+            devs.append(d)
+        prof = L.RfProfile()
+        lib.rf_profile_end(store._ptr, ctypes.byref(prof))
+        print(json.dumps({"mode": label, "wall_ms": round(sum(walls) / steps, 3),
+                          "event_ms": round(sum(devs) / steps, 3),
+                          "fuse_ms": round(prof.fuse_ms / steps, 3),
+                          "check_ms": round(prof.check_ms / steps, 3),
+                          "footprint_ms": round(prof.footprint_ms / steps, 3),
+                          "other_ms": round(prof.other_ms / steps, 3)}), flush=True)
+
+    phase("resident")
+    host = {id(kf): kf.to_host(pinned=True) for kf in kfs}
+    for e in scen.ledger.entries:
+        e.kf = host[id(e.kf)]
+    phase("host")
+    for e in scen.ledger.entries:
+        e.kf = kfs[e.kf_id - 1]
+    phase("resident")
+
+
+if __name__ == "__main__":
+    main()
