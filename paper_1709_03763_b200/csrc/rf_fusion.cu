@@ -412,23 +412,6 @@ struct PwNode {
   double val;
 };
 
-// Leaves of the pairwise tree (numpy's blocks of <= 128), all in parallel.
-__global__ void k_pairwise_leaves(const double* a, const PwNode* nodes, int n_leaves, double* val) {
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < n_leaves) val[k] = pairwise_leaf(a + nodes[k].off, nodes[k].n);
-}
-
-// Internal nodes level by level (nodes sorted by height, children first):
-// one CTA, a barrier per level -- the additions are numpy's, in its order.
-__global__ void __launch_bounds__(1024) k_pairwise_levels(const PwNode* nodes, const int* level_off,
-                                                          int n_levels, double* val, double* out) {
-  for (int l = 1; l < n_levels; ++l) {
-    for (int k = level_off[l] + threadIdx.x; k < level_off[l + 1]; k += blockDim.x)
-      val[k] = val[nodes[k].left] + val[nodes[k].right];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = val[level_off[n_levels] - 1];
-}
 
 // blurriness (:310-332): scores (s_f - v.sum()) / s_f per axis with s_f > 0
 __global__ void k_blur_finish(const double* sums, int n_axes, double* blur_weight) {
@@ -692,16 +675,6 @@ rf_status pairwise_sums(int count, const double* const* a, const long long* n, d
   return RF_OK;
 }
 
-rf_status pairwise_sum(const double* a, long long n, double* out, cudaStream_t s) {
-  const PwTree* t = pairwise_tree(n);
-  if (!t) return RF_CUDA;
-  double* val = nullptr;
-  if (cudaMallocAsync(&val, sizeof(double) * t->n_nodes, s) != cudaSuccess) return RF_CUDA;
-  k_pairwise_leaves<<<(t->n_leaves + 127) / 128, 128, 0, s>>>(a, t->nodes, t->n_leaves, val);
-  k_pairwise_levels<<<1, 1024, 0, s>>>(t->nodes, t->level_off, t->n_levels, val, out);
-  cudaFreeAsync(val, s);
-  return RF_OK;
-}
 
 // The stream-ordered pool keeps what it allocated between calls (the fusion
 // entry points allocate scratch per call; releasing it at every host sync
