@@ -213,8 +213,8 @@ def run_b200(args):
     # inboxes (rf_route).  Off by default: on this workload the replicated
     # sampling with its footprint memo costs less per shard.
     routed = world > 1 and os.environ.get("RF_ROUTE", "0") == "1"
-    if routed:
-        V.connect_shards_distributed(store, cfg)
+    if world > 1:  # errors agreed across shards on every call (+ routing if asked)
+        V.connect_shards_distributed(store, cfg, route=routed)
     n_events = args.warmup + 2 * args.steps + 2
     scen = Scenario(R, G, SY, gt_kf, drifted, keyframes,
                     make_events((n_kf + EVENT_EVERY_KF - 1) // EVENT_EVERY_KF, n_events))

@@ -345,9 +345,12 @@ class TwoTierStore:
         their owners, wait for every shard to have routed, run the op, then
         agree on failure (an error on any shard raises on all of them)."""
         r = self._router
-        st = self._call_status("rf_route", n_ops, views, poses, centers)
-        r.barrier()  # every shard's footprints are in the inboxes
-        if st == L.RF_OK:
+        if r.routed:
+            st = self._call_status("rf_route", n_ops, views, poses, centers)
+            r.barrier()  # every shard's footprints are in the inboxes
+            if st == L.RF_OK:
+                st = self._call_status(name, *args)
+        else:  # replicated sampling: only the status agreement
             st = self._call_status(name, *args)
         worst = r.agree(st)
         _check(self._ptr, st, name)
@@ -618,7 +621,7 @@ def correct_windows(store, windows, cfg, next_center=None):
     (rf_correct_windows) and ONE host synchronisation for all of them.
     Advances entry.integrated_pose exactly where the sequential reference
     calls would have; raises the reference's exceptions."""
-    if store._router is None:
+    if store._router is None or not store._router.routed:
         return _correct_windows(store, windows, cfg, next_center)
     # routed shards: as many windows per native call as the inboxes hold
     # (every shard makes the same split)
@@ -670,6 +673,9 @@ def _correct_windows(store, windows, cfg, next_center=None):
         if store._router is None:
             store._call("rf_correct_windows", len(windows), sizes, views, olds, news, nc,
                         ctypes.byref(res))
+        elif not store._router.routed:
+            store._routed_call("rf_correct_windows", 0, None, None, None, len(windows), sizes,
+                               views, olds, news, nc, ctypes.byref(res))
         else:  # per window: its m removal footprints, then its m integration ones
             nr = 2 * n
             rv, rp = (L.RfKfView * nr)(), (L.RfPose * nr)()
@@ -714,10 +720,11 @@ class _ShardRouter:
     the shards (after every shard routed a call's footprints into the
     owners' inboxes) and an agreement on the call's status."""
 
-    def __init__(self, max_ops, barrier, agree):
+    def __init__(self, max_ops, barrier, agree, routed=True):
         self.max_ops = max_ops
         self.barrier = barrier
         self.agree = agree
+        self.routed = routed
 
 
 class _ThreadGroup:
@@ -747,7 +754,8 @@ def _route_setup(store, max_ops, cap_keys):
     return inbox.value
 
 
-def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), timeout=300.0):
+def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), timeout=300.0,
+                   route=True):
     """Route the footprints of G shard stores living in ONE process (one
     device or several; each shard is then driven from its own thread, e.g.
     tests and single-process drivers).  Every integrate / deintegrate /
@@ -757,12 +765,17 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
     if G < 2 or any(s.shard_count != G for s in stores) or \
             sorted(s.shard_rank for s in stores) != list(range(G)):
         raise ValueError("connect_shards needs one store per shard rank 0..G-1")
-    cap = cap_keys or _route_cap(G, image)
     for s in stores:
         s._bind(cfg)
+    group = _ThreadGroup(G, timeout)
+    if not route:  # replicated sampling: only the status agreement
+        for s in stores:
+            s._router = _ShardRouter(max_ops, group.bar.wait, (lambda rank: lambda code:
+                                     group.agree(rank, code))(s.shard_rank), routed=False)
+        return
+    cap = cap_keys or _route_cap(G, image)
     inbox = {s.shard_rank: _route_setup(s, max_ops, cap) for s in stores}
     arr = (ctypes.c_void_p * G)(*[inbox[r] for r in range(G)])
-    group = _ThreadGroup(G, timeout)
     for s in stores:
         s._call("rf_route_connect", arr)
         s._router = _ShardRouter(max_ops, group.bar.wait,
@@ -770,13 +783,28 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
 
 
 def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640, 480),
-                               group=None):
+                               group=None, route=True):
     """One shard per process (one GPU each) under torch.distributed: the
     inboxes are exchanged once as CUDA IPC handles; the per-call barrier and
-    status agreement are torch.distributed collectives."""
+    status agreement are torch.distributed collectives.  route=False keeps the
+    replicated sampling and installs only the status agreement (an error on
+    any shard raises on every shard)."""
     import torch
     import torch.distributed as dist
 
+    dev = torch.device("cuda", store.device if store.device is not None
+                       else torch.cuda.current_device())
+
+    def agree(code):
+        t = torch.tensor([int(code)], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        return int(t.item())
+
+    if not route:
+        store._bind(cfg)
+        store._router = _ShardRouter(max_ops, lambda: dist.barrier(group=group), agree,
+                                     routed=False)
+        return
     G = store.shard_count
     cap = cap_keys or _route_cap(G, image)
     store._bind(cfg)
@@ -786,13 +814,6 @@ def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640
     handles = [None] * G
     dist.all_gather_object(handles, bytes(h), group=group)
     store._call("rf_route_ipc_open", ctypes.c_char_p(b"".join(handles)))
-    dev = torch.device("cuda", store.device)
-
-    def agree(code):
-        t = torch.tensor([int(code)], dtype=torch.int32, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-        return int(t.item())
-
     store._router = _ShardRouter(max_ops, lambda: dist.barrier(group=group), agree)
 
 

@@ -204,3 +204,27 @@ def test_routed_call_without_route_is_rejected(V):
                         None, 0)
     assert st == L.RF_INVALID_ARG
     del keep
+
+
+@pytest.mark.parametrize("route", [True, False])
+def test_shard_local_inconsistency_raises_everywhere(V, route):
+    """A de-integration at a pose the keyframe was never integrated at fails
+    on the shards owning the failing blocks; with the shards connected, every
+    shard raises VolumeInconsistencyError (routed or replicated sampling)."""
+    from paper_1709_03763_b200.errors import VolumeInconsistencyError
+
+    cfg = V.VolumeConfig(voxel_size=0.005, mu=0.06, stream_radius=6.0, hash_buckets=1 << 15)
+    frames, old, _ = scene(13, n=1)
+    G = 2
+    shards = [V.TwoTierStore(block_capacity=1 << 16, shard_rank=r, shard_count=G)
+              for r in range(G)]
+    V.connect_shards(shards, cfg, image=(320, 240), route=route)
+    wrong = S.SPose(S.rot_z(0.3), [0.05, 0.02, 0.1])
+
+    def run(r, s):
+        V.stream(s, old[0].translation, cfg)
+        V.integrate(s, frames[0], old[0], cfg)
+        V.deintegrate(s, frames[0], wrong, cfg)
+
+    out = lockstep(shards, run)
+    assert all(isinstance(e, VolumeInconsistencyError) for e in out), out
