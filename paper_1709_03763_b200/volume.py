@@ -209,7 +209,8 @@ def kf_view(kf, device=0):
     keyframes every call.  In-place edits of a plane keep its pointer; the
     footprint memo's content hash covers those."""
     intr = kf.intrinsics
-    ident = (id(kf.depth), id(kf.weight), id(getattr(kf, "color", None)), id(intr), device)
+    ident = (id(kf.depth), id(kf.weight), id(getattr(kf, "color", None)), device,
+             intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
     try:
         hit = _VIEWS.get(kf)
     except TypeError:  # not weak-referenceable: no memo
