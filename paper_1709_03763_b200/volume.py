@@ -210,7 +210,8 @@ def kf_view(kf, device=0):
     footprint memo's content hash covers those."""
     intr = kf.intrinsics
     ident = (id(kf.depth), id(kf.weight), id(getattr(kf, "color", None)), device,
-             intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height)
+             intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height,
+             getattr(kf, "memo_tag", 0))
     try:
         hit = _VIEWS.get(kf)
     except TypeError:  # not weak-referenceable: no memo

@@ -43,3 +43,31 @@ def test_pose_copy_is_independent():
     q = p.copy()
     q.translation[0] = 9.0
     assert p.translation[0] == 1.0 and np.array_equal(q.rotation, p.rotation)
+
+
+def test_views_are_memoised_per_keyframe_planes():
+    """A correction re-marshals the same keyframes: the view of a keyframe is
+    reused while its planes are the same objects (in-place edits keep the
+    pointers), rebuilt when a plane is replaced, and never memoised when the
+    planes had to be converted (a copy would go stale)."""
+    rng = np.random.default_rng(5)
+    f = S.random_frame(rng)
+    v1, _ = V.kf_view(f, device=0)
+    v2, _ = V.kf_view(f, device=0)
+    assert v1 is v2
+    f.depth = f.depth.copy()
+    v3, _ = V.kf_view(f, device=0)
+    assert v3 is not v1 and v3.depth == f.depth.ctypes.data
+    g = S.random_frame(rng)
+    g.depth = g.depth.astype(np.float32)
+    w1, _ = V.kf_view(g, device=0)
+    w2, _ = V.kf_view(g, device=0)
+    assert w1 is not w2  # converted plane: a fresh copy every call
+
+
+def test_memo_tag_travels_to_the_view():
+    rng = np.random.default_rng(6)
+    f = S.random_frame(rng)
+    f.memo_tag = 12345
+    view, _ = V.kf_view(f, device=0)
+    assert view.memo_tag == 12345
