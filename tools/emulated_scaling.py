@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--keyframes", type=int, default=400)
     ap.add_argument("--steps", type=int, default=6)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--voxel", type=float, default=None, help="voxel size (default: bench's)")
     args = ap.parse_args()
 
     import torch
@@ -62,13 +63,14 @@ def main():
         kf.pose = drifted[k]
         kfs.append(kf)
     torch.cuda.synchronize()
-    cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
-                         hash_buckets=1 << 21)
+    voxel = args.voxel or B.VOXEL
+    cfg = V.VolumeConfig(voxel_size=voxel, mu=B.MU, stream_radius=B.RADIUS,
+                         hash_buckets=1 << 22 if voxel < B.VOXEL else 1 << 21)
     n_anchors = (args.keyframes + B.EVENT_EVERY_KF - 1) // B.EVENT_EVERY_KF
     events = B.make_events(n_anchors, args.warmup + 2 * args.steps + 2)
 
     def run(G, mode):
-        cap = 2_600_000 // G + 200_000
+        cap = int(2_600_000 * (B.VOXEL / voxel) ** 3) // G + 200_000
         stores = [V.TwoTierStore(block_capacity=cap, shard_rank=r, shard_count=G)
                   for r in range(G)]
         if G > 1 and mode == "routed":
