@@ -1167,7 +1167,11 @@ rf_status rf_route(rf_volume* v, int32_t n, const rf_kf_view* kfs, const rf_pose
     const long long tiles = static_cast<long long>((kf->width + kTile - 1) / kTile) *
                             ((kf->height + kTile - 1) / kTile);
     const long long mine = (tiles + v->cfg.shard_count - 1) / v->cfg.shard_count;
-    const int grid = static_cast<int>(std::max(1LL, std::min<long long>(mine, v->fp_grid_cap)));
+    // enough CTAs to fill the GPU (8 per SM): split each tile by step range
+    r.parts = static_cast<int>(std::max(1LL, std::min<long long>(
+        std::min(8, fp.n_steps), v->fp_grid_cap / std::max(1LL, mine))));
+    const int grid = static_cast<int>(
+        std::max(1LL, std::min<long long>(mine * r.parts, v->fp_grid_cap)));
     ProfScope ps(v, 2);
     launch(k_route, grid, 256, 0, v->stream, fp, r);
     if (v->profiling) v->prof_launches += 1;
