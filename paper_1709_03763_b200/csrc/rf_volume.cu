@@ -487,10 +487,7 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
   v->memo_free.pop_back();
   char* mem = v->memo_arena + static_cast<size_t>(index) * v->memo_slot_bytes;
   FpEntry* dev = reinterpret_cast<FpEntry*>(mem);
-  // initialise the descriptor on the stream (a pageable host->device copy
-  // would synchronise the host with the stream mid-batch)
-  launch(k_memo_init, 1, 1, 0, v->stream, dev, reinterpret_cast<long long*>(mem + head),
-         v->memo_slot_cap);
+  // (its descriptor is initialised by the op's k_footprint: memo_fresh)
   v->memo_lru.push_front(key);
   MemoSlot ms;
   ms.dev = dev;
@@ -658,6 +655,12 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     fp.route_cap = L.cap;
   } else {
     memo = memo_lookup(v, kf, pose, existed);
+    if (memo) {
+      fp.memo_keys = reinterpret_cast<long long*>(reinterpret_cast<char*>(memo) +
+                                                  ((sizeof(FpEntry) + 15) & ~size_t(15)));
+      fp.memo_cap = v->memo_slot_cap;
+      fp.memo_fresh = existed ? 0 : 1;
+    }
   }
   int launches = 0;
   {
