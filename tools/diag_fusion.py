@@ -1,3 +1,5 @@
+"""Host/device profile of fuse_depth on corridor frames (cProfile of the
+Python path; the wall time per frame).  Diagnostic only."""
 import cProfile, pstats, sys, os, time
 sys.path.insert(0, os.getcwd())
 import torch
