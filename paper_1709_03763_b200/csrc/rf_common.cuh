@@ -24,10 +24,7 @@ constexpr long long kNoKey = 0x7fffffffffffffffLL;
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kFuseThreads = 256;
 // touched-list entry: slot | kNewFlag (the op created the block: all zero)
-// | kAlsoInt (merged removal + integration: the block is also in the
-// integration's footprint, rf_volume.cu op_fuse)
 constexpr unsigned kNewFlag = 0x80000000u;
-constexpr unsigned kAlsoInt = 0x40000000u;
 constexpr unsigned kSlotMask = 0x3fffffffu;
 
 enum ErrKind : int { kErrNone = 0, kErrContract = 1, kErrInconsistent = 2, kErrCapacity = 3 };
@@ -90,11 +87,7 @@ struct OpCounters {
   // index 0 the removal check, 1 integrate / removal, 2 the fix-up
   unsigned n_defer[3];
   unsigned done_ctas[3];
-  // merged removal + integration (the integration op's record): footprint
-  // blocks already in the removal's list, and voxels the merged kernel moved
-  unsigned long long n_shared;
-  unsigned long long voxels_union;
-  unsigned capture_n;  // merged kernel: memo keys written so far
+  unsigned capture_n;  // sharded footprint: memo keys written so far
   unsigned next_block[3];  // fuse kernels: dynamic block queue (per defer index)
   unsigned fp_done;        // footprint kernel: finished CTAs
 };
@@ -126,7 +119,7 @@ struct Table {
   double* pool;
   int* free_stack;
   int* returned;
-  int* touched;   // slot | kNewFlag | kAlsoInt
+  int* touched;   // slot | kNewFlag
   int* tpos;      // per slot: its index in the current touched list
   long long* touched_keys;  // packed key of touched[i] (fuse reads no keys[] indirection)
   int* new_list;  // slots created by the current op

@@ -23,7 +23,6 @@
 
 #include "refusion_b200.h"
 #include "rf_kernels.cuh"
-#include "rf_fuse_legacy.cuh"
 #include "rf_mesh.cuh"
 
 #include <cub/cub.cuh>
@@ -32,7 +31,9 @@ using namespace rf;
 
 namespace {
 
-constexpr int kMaxWindowOps = 4096;
+// entries of one rf_correct_windows call (the Python layer splits bigger
+// batches at window boundaries, volume.MAX_CALL_ENTRIES)
+constexpr int kMaxWindowOps = 16384;
 // distinct new blocks one (de)integration may create (load factor stays low)
 constexpr int kPendingSlots = 1 << 20;
 // tile keys beyond a tile's shared-memory list (only pathological tiles)
@@ -97,10 +98,6 @@ struct rf_volume {
   int n_sms = 148;
   int fuse_grid = 148 * 2;
   int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
-  int legacy_grids[4] = {148, 148, 148, 148};
-  bool legacy_fuse = false;  // RF_FUSE_IMPL=legacy: whole-block-prefetch A/B baseline
-  int merged_grid = 148;
-  bool merge_pairs = false;  // RF_MERGE_PAIRS=1 enables k_fuse_merged
   // staging of host keyframe planes (rf_kf_view.planes_on_host)
   struct StageSlot {
     double* buf = nullptr;
@@ -198,8 +195,7 @@ double sqrt_le_bound(double r) {
 
 // Launch a batch kernel with programmatic stream serialization (PDL): its
 // CTAs may be scheduled while the previous kernel drains; every batch kernel
-// starts with griddep_wait().  RF_PDL=0 turns it off (A/B).
-bool g_pdl = true;
+// starts with griddep_wait().
 
 template <typename... KArgs, typename... Args>
 void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
@@ -213,7 +209,7 @@ void launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaSt
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = g_pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
@@ -247,7 +243,6 @@ struct OpInfo {
   int kind;  // 0 stream, 1 integrate, 2 deintegrate, 3 gc, 4 allocate
   int entry;
   int window = 0;
-  bool merged = false;  // fused by k_fuse_merged with its neighbour
 };
 
 struct Batch {
@@ -260,11 +255,6 @@ struct Batch {
   std::vector<OpInfo> infos;
   std::vector<FuseParams> fparams;  // per op (fuse ops only)
   int gc_op = -1;
-  // a de-integration whose removal is deferred into the next integration's
-  // merged kernel (op index, its params and footprint epoch)
-  int pending_rm = -1;
-  FuseParams pending_p{};
-  unsigned pending_epoch = 0;
   // routed volume: next inbox op to consume (route_force >= 0 overrides)
   int route_next = 0;
   int route_force = -1;
@@ -519,13 +509,10 @@ struct RouteConsume {
   }
 };
 
-// Launch the batched fuse kernel of mode kMode (or the legacy A/B baseline).
+// Launch the batched fuse kernel of mode kMode.
 template <int kMode>
 void launch_fuse(rf_volume* v, const FuseParams& p) {
-  if (v->legacy_fuse)
-    launch(k_fuse_legacy<kMode>, v->legacy_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
-  else
-    launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
+  launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
 }
 
 // Host keyframe planes (planes_on_host): copy each distinct keyframe of a
@@ -625,23 +612,13 @@ void wait_color(rf_volume* v, const rf_kf_view* kf) {
   if (it != v->color_ready.end()) cudaStreamWaitEvent(v->stream, it->second, 0);
 }
 
-// mode: 0 integrate, 1 deintegrate, 2 allocate only.  defer_removal (mode
-// 1): run the removal check now but leave the removal to the next op, which
-// must be an integration called with merge = true: the two become one
-// k_fuse_merged launch over the union of their footprints (the stream ops
-// between them move no data, so per voxel the order is unchanged).
-void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry,
-             bool defer_removal = false, bool merge = false) {
+// mode: 0 integrate, 1 deintegrate, 2 allocate only.
+void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
   if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
-  merge = merge && mode == 0 && b.pending_rm >= 0 && v->cfg.shard_count == 1;
-  if (merge) {
-    fp.merge_op = v->d_ops + b.pending_rm;
-    fp.merge_epoch = b.pending_epoch;
-  }
   bool existed = false;
   FpEntry* memo = nullptr;
   if (v->route_on) {  // the footprint arrives in this shard's inbox (k_route)
@@ -696,17 +673,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     return;
   }
   if (mode == 0) wait_color(v, kf);
-  if (mode == 0 && merge) {
-    {
-      ProfScope ps(v, 0);
-      launch(k_fuse_merged, v->merged_grid, kFuseThreads, kMergedSmemBytes, v->stream, v->T,
-             b.pending_p, p);
-    }
-    b.infos[b.pending_rm].merged = true;
-    b.infos[op].merged = true;
-    b.pending_rm = -1;
-    launches += 1;
-  } else if (mode == 0) {
+  if (mode == 0) {
     ProfScope ps(v, 0);
     launch_fuse<kIntegrate>(v, p);
     launches += 1;
@@ -718,11 +685,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     p.capture = nullptr;
     launches += 1;
     wait_color(v, kf);  // the check read no colour; the removal does
-    if (defer_removal && v->merge_pairs && !v->legacy_fuse && v->cfg.shard_count == 1) {
-      b.pending_rm = op;
-      b.pending_p = p;
-      b.pending_epoch = fp.epoch;
-    } else {
+    {
       ProfScope ps(v, 0);
       launch_fuse<kApplyRemove>(v, p);
       launches += 1;
@@ -731,19 +694,8 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   if (v->profiling) v->prof_launches += launches;
 }
 
-// A deferred removal whose integration never came (not produced by the
-// callers, kept for safety): run it on its own.
-void flush_pending(Batch& b) {
-  if (b.pending_rm < 0) return;
-  rf_volume* v = b.v;
-  ProfScope ps(v, 0);
-  launch_fuse<kApplyRemove>(v, b.pending_p);
-  b.pending_rm = -1;
-}
-
 void op_gc(Batch& b) {
   rf_volume* v = b.v;
-  flush_pending(b);
   const int op = next_op(b);
   b.infos.push_back({3, -1});
   b.fparams.emplace_back();
@@ -768,7 +720,6 @@ struct BatchOutcome {
 // the ops that executed.
 rf_status batch_end(Batch& b, BatchOutcome& out) {
   rf_volume* v = b.v;
-  flush_pending(b);
   const int n = std::max(b.n_ops, 1);
   cudaMemcpyAsync(v->h_ops, v->d_ops, sizeof(OpCounters) * n, cudaMemcpyDeviceToHost, v->stream);
   cudaMemcpyAsync(v->h_ws, v->d_ws, sizeof(WinState), cudaMemcpyDeviceToHost, v->stream);
@@ -794,11 +745,9 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
     for (int i = 0; i < b.n_ops; ++i) {
       const int k = b.infos[i].kind;
       if ((k == 1 || k == 2) && (!out.err_kind || i < out.err_op)) {
-        // a merged pair moves each voxel of the union once
         const OpCounters& o = v->h_ops[i];
-        if (!b.infos[i].merged) v->prof_voxels += static_cast<long long>(o.voxels_updated);
-        else if (k == 1) v->prof_voxels += static_cast<long long>(o.voxels_union);
-        v->prof_blocks += static_cast<long long>(o.n_touched + (k == 1 ? o.n_shared : 0));
+        v->prof_voxels += static_cast<long long>(o.voxels_updated);
+        v->prof_blocks += static_cast<long long>(o.n_touched);
       }
     }
   }
@@ -896,22 +845,6 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, 0);
   for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse_legacy<kIntegrate>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse_legacy<kCheckRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse_legacy<kApplyRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse_legacy<kRemoveReadd>, kFuseThreads, 0);
-  for (int m = 0; m < 4; ++m) v->legacy_grids[m] = v->n_sms * std::max(occ[m], 1);
-  cudaFuncSetAttribute(k_fuse_merged, cudaFuncAttributeMaxDynamicSharedMemorySize, kMergedSmemBytes);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse_merged, kFuseThreads, kMergedSmemBytes);
-  v->merged_grid = v->n_sms * std::max(occ[0], 1);
-  {
-    const char* impl = std::getenv("RF_FUSE_IMPL");
-    v->legacy_fuse = impl && std::string(impl) == "legacy";
-    const char* pdl = std::getenv("RF_PDL");
-    g_pdl = !(pdl && std::string(pdl) == "0");
-    const char* mp = std::getenv("RF_MERGE_PAIRS");
-    v->merge_pairs = mp && std::string(mp) == "1";
-  }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
   const size_t cap = static_cast<size_t>(cfg->block_capacity);
@@ -1276,7 +1209,8 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     if (sizes[w] < 0) return RF_INVALID_ARG;
     total += sizes[w];
   }
-  if (total > kMaxWindowOps) return fail(v, RF_INVALID_ARG, "too many entries in one call");
+  if (total > kMaxWindowOps || n_windows > kMaxWindowOps)
+    return fail(v, RF_INVALID_ARG, "too many entries in one call");
   if (total > 0 && (!kfs || !old_poses || !new_poses)) return RF_INVALID_ARG;
   for (long long i = 0; i < total; ++i)
     if (!valid_kf(&kfs[i])) return RF_INVALID_ARG;
@@ -1310,14 +1244,13 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     op_stream(b, o[0].t);
     for (int i = 0; i < m; ++i) {
       op_stream(b, o[i].t);
-      // the window's last removal merges with its first integration
-      op_fuse(b, &k[i], &o[i], 1, i, /*defer_removal=*/i == m - 1);
+      op_fuse(b, &k[i], &o[i], 1, i);
       b.infos.back().window = w;
     }
     op_stream(b, n[0].t);
     for (int i = 0; i < m; ++i) {
       op_stream(b, n[i].t);
-      op_fuse(b, &k[i], &n[i], 0, i, false, /*merge=*/i == 0);
+      op_fuse(b, &k[i], &n[i], 0, i);
       b.infos.back().window = w;
       stage_consumed(v, slot_of, i);  // last use of its planes
     }
@@ -1333,8 +1266,7 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
     if (out.err_kind && i > out.err_op) break;
     const OpInfo& inf = b.infos[i];
     if (inf.kind == 1 || inf.kind == 2) {
-      r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched +
-                                               (inf.kind == 1 ? v->h_ops[i].n_shared : 0));
+      r.blocks_touched += static_cast<int64_t>(v->h_ops[i].n_touched);
       r.n_new += static_cast<int64_t>(v->h_ops[i].n_new);
       if (inf.kind == 1) r.voxels_updated += static_cast<int64_t>(v->h_ops[i].voxels_updated);
     } else if (inf.kind == 3) {

@@ -15,6 +15,8 @@ import numpy as np
 
 ORTHONORMAL_TOL = 1e-6
 DEFAULT_DISTANCE_SCALE = np.array([2.0, 2.0, 2.0, 1.0, 1.0, 1.0])
+_EYE3 = np.eye(3)
+_EYE3.flags.writeable = False
 
 
 @dataclass
@@ -43,10 +45,21 @@ class Pose:
     def __post_init__(self):
         self.rotation = np.asarray(self.rotation, dtype=np.float64)
         self.translation = np.asarray(self.translation, dtype=np.float64).reshape(3)
-        err = np.abs(self.rotation.T @ self.rotation - np.eye(3)).max()
+        R = self.rotation
+        err = np.abs(R.T @ R - _EYE3).max()
         if err > ORTHONORMAL_TOL:
             raise ValueError(f"rotation not orthonormal (err={err:.2e})")
-        if abs(np.linalg.det(self.rotation) - 1.0) > ORTHONORMAL_TOL:
+        # the determinant test of geometry.py:52-53: a cofactor expansion
+        # decides it, except within 1e-9 of the tolerance, where LAPACK's LU
+        # determinant (the reference's np.linalg.det) does
+        if R.shape == (3, 3):
+            (a, b, c), (d, e, f), (g, h, i) = R.tolist()
+            dev = abs(a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g) - 1.0)
+            if abs(dev - ORTHONORMAL_TOL) < 1e-9:
+                dev = abs(np.linalg.det(R) - 1.0)
+        else:
+            dev = abs(np.linalg.det(R) - 1.0)
+        if dev > ORTHONORMAL_TOL:
             raise ValueError("rotation must have determinant +1")
 
     @classmethod
@@ -58,6 +71,9 @@ class Pose:
         out = object.__new__(Pose)
         out.rotation = self.rotation.copy()
         out.translation = self.translation.copy()
+        memo = self.__dict__.get("_rf_euler")
+        if memo is not None:
+            out._rf_euler = memo
         return out
 
 
@@ -109,9 +125,25 @@ def wrap_angle(a):
     return np.pi - np.mod(np.pi - np.asarray(a, dtype=np.float64), 2.0 * np.pi)
 
 
+def _euler_of(pose):
+    """euler_zyx(pose.rotation), memoised on the pose object while its
+    rotation holds the same bits."""
+    rb = pose.rotation.tobytes()
+    memo = pose.__dict__.get("_rf_euler")
+    if memo is not None and memo[0] == rb:
+        return memo[1]
+    e = euler_zyx(pose.rotation)
+    e.flags.writeable = False
+    try:
+        pose._rf_euler = (rb, e)
+    except AttributeError:
+        pass
+    return e
+
+
 def pose_distance(T, U, s=DEFAULT_DISTANCE_SCALE):
     """Scaled norm of (wrapped Euler difference, translation difference)."""
-    ea, eb = euler_zyx(T.rotation), euler_zyx(U.rotation)
+    ea, eb = _euler_of(T), _euler_of(U)
     d = np.concatenate([wrap_angle(ea - eb), T.translation - U.translation])
     return float(np.linalg.norm(np.asarray(s, dtype=np.float64) * d))
 

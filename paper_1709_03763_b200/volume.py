@@ -40,6 +40,8 @@ _PACK_BIAS = 1 << 20
 _PACK_SPAN = 1 << 21
 
 DEFAULT_BLOCK_CAPACITY = int(os.environ.get("REFUSION_B200_BLOCKS", str(1 << 16)))
+MAX_CALL_ENTRIES = 4096     # entries per native correction call (split above)
+MAX_WINDOW_ENTRIES = 16384  # rf_correct_windows' kMaxWindowOps: one window never splits
 
 
 @dataclass(frozen=True)
@@ -200,7 +202,11 @@ def _host_plane(arr, shape):
     return a.ctypes.data, a
 
 
-_VIEWS = weakref.WeakKeyDictionary()  # keyframe -> (plane identities, device, view, keep)
+# keyframe id -> (plane identities, view, keep); an entry is dropped when its
+# keyframe dies (weakref.finalize), so ids are never confused.  Keyed by id
+# because keyframes are usually unhashable (keyframe_fusion.Keyframe is a
+# plain dataclass).
+_VIEWS = {}
 
 
 def kf_view(kf, device=0):
@@ -212,10 +218,8 @@ def kf_view(kf, device=0):
     ident = (id(kf.depth), id(kf.weight), id(getattr(kf, "color", None)), device,
              intr.fx, intr.fy, intr.cx, intr.cy, intr.width, intr.height,
              getattr(kf, "memo_tag", 0))
-    try:
-        hit = _VIEWS.get(kf)
-    except TypeError:  # not weak-referenceable: no memo
-        return kf_view_uncached(kf, device)
+    key = id(kf)
+    hit = _VIEWS.get(key)
     if hit is not None and hit[0] == ident:
         return hit[1], hit[2]
     v, keep = kf_view_uncached(kf, device)
@@ -227,7 +231,12 @@ def kf_view(kf, device=0):
         own.append(_own_ptr(kf.color))
         ptrs.append(v.color)
     if all(o is not None and o == p for o, p in zip(own, ptrs)):
-        _VIEWS[kf] = (ident, v, keep)
+        try:
+            if key not in _VIEWS:
+                weakref.finalize(kf, _VIEWS.pop, key, None)
+            _VIEWS[key] = (ident, v, keep)
+        except TypeError:  # not weak-referenceable: no memo
+            pass
     return v, keep
 
 
@@ -623,23 +632,31 @@ def correct_windows(store, windows, cfg, next_center=None):
     (rf_correct_windows) and ONE host synchronisation for all of them.
     Advances entry.integrated_pose exactly where the sequential reference
     calls would have; raises the reference's exceptions."""
-    if store._router is None or not store._router.routed:
-        return _correct_windows(store, windows, cfg, next_center)
-    # routed shards: as many windows per native call as the inboxes hold
-    # (every shard makes the same split)
-    per = store._router.max_ops // 2
     windows = [list(w) for w in windows]
-    if any(len(w) > per for w in windows):
-        raise ValueError(f"a window of more than {per} entries exceeds the routed inboxes "
-                         f"(connect_shards max_ops={store._router.max_ops})")
+    if store._router is None or not store._router.routed:
+        # one native call holds up to MAX_CALL_ENTRIES entries (and windows);
+        # bigger batches are split at window boundaries (windows run in
+        # order either way)
+        per = MAX_CALL_ENTRIES
+        if any(len(w) > MAX_WINDOW_ENTRIES for w in windows):
+            raise ValueError(f"a correction window of more than {MAX_WINDOW_ENTRIES} entries")
+    else:
+        # routed shards: as many windows per native call as the inboxes hold
+        # (every shard makes the same split)
+        per = store._router.max_ops // 2
+        if any(len(w) > per for w in windows):
+            raise ValueError(f"a window of more than {per} entries exceeds the routed inboxes "
+                             f"(connect_shards max_ops={store._router.max_ops})")
     chunks, cur, used = [], [], 0
     for w in windows:
-        if cur and used + len(w) > per:
+        if cur and (used + len(w) > per or len(cur) >= MAX_CALL_ENTRIES):
             chunks.append(cur)
             cur, used = [], 0
         cur.append(w)
         used += len(w)
     chunks.append(cur)
+    if len(chunks) == 1:
+        return _correct_windows(store, chunks[0], cfg, next_center)
     done = 0
     for ci, ch in enumerate(chunks):
         done += _correct_windows(store, ch, cfg, next_center if ci == len(chunks) - 1 else None)
@@ -874,7 +891,8 @@ def load_volume(path, block_capacity=None, device=None):
         recs = np.fromfile(fh, dtype=_RECORD, count=count)
     if len(recs) != count:
         raise ValueError(f"truncated snapshot: {len(recs)} of {count} blocks")
-    store = TwoTierStore(block_capacity=block_capacity or max(count, DEFAULT_BLOCK_CAPACITY),
+    # headroom: the loaded volume keeps growing (the pool itself never does)
+    store = TwoTierStore(block_capacity=block_capacity or max(2 * count, DEFAULT_BLOCK_CAPACITY),
                          device=device)
     if count:
         data = np.ascontiguousarray(np.transpose(recs["rec"], (0, 2, 1)))

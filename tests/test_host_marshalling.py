@@ -71,3 +71,49 @@ def test_memo_tag_travels_to_the_view():
     f.memo_tag = 12345
     view, _ = V.kf_view(f, device=0)
     assert view.memo_tag == 12345
+
+
+def test_views_are_memoised_for_unhashable_keyframes():
+    """keyframe_fusion.Keyframe is a plain (unhashable) dataclass: its views
+    are memoised too, and dropped when the keyframe dies."""
+    import gc
+
+    from paper_1709_03763_b200.keyframe_fusion import Keyframe
+
+    rng = np.random.default_rng(7)
+    f = S.random_frame(rng)
+    kf = Keyframe(intrinsics=f.intrinsics, pose=Pose.identity(), anchor_id=0,
+                  rel_pose=Pose.identity(), depth=f.depth, weight=f.weight, color=f.color)
+    v1, _ = V.kf_view(kf, device=0)
+    v2, _ = V.kf_view(kf, device=0)
+    assert v1 is v2
+    key = id(kf)
+    assert key in V._VIEWS
+    del kf, v1, v2
+    gc.collect()
+    assert key not in V._VIEWS
+
+
+def test_correction_batches_split_at_window_boundaries():
+    """More entries than one native call holds are split into chunks of whole
+    windows (finalize over > 4096 moved keyframes)."""
+    calls = []
+
+    class _Store:
+        _router = None
+
+    def fake(store, windows, cfg, next_center=None):
+        calls.append(([len(w) for w in windows], next_center))
+        return sum(len(w) for w in windows)
+
+    orig = V._correct_windows
+    V._correct_windows = fake
+    try:
+        windows = [[object()] * 10 for _ in range(1000)]
+        n = V.correct_windows(_Store(), windows, None, next_center="c")
+    finally:
+        V._correct_windows = orig
+    assert n == 10_000
+    assert all(sum(sizes) <= V.MAX_CALL_ENTRIES for sizes, _ in calls)
+    assert [c for _, c in calls] == [None] * (len(calls) - 1) + ["c"]
+    assert sum(len(s) for s, _ in calls) == 1000

@@ -427,49 +427,6 @@ def test_window_integration_contract_error_matches_oracle(V):
     assert_same_state(store, ref)
 
 
-@pytest.fixture()
-def merged_pairs(monkeypatch):
-    """Volumes created under this fixture run each window's last removal and
-    first integration as one k_fuse_merged launch (RF_MERGE_PAIRS=1)."""
-    monkeypatch.setenv("RF_MERGE_PAIRS", "1")
-
-
-def test_merged_pairs_window_bitexact(V, merged_pairs):
-    test_vga_window_correction_bitexact(V)
-
-
-def test_merged_pairs_contract_error(V, merged_pairs):
-    test_window_integration_contract_error_matches_oracle(V)
-
-
-def test_merged_pairs_extreme_values(V, merged_pairs):
-    """Deferred voxels of the merged kernel: both parts (removal, then
-    integration) re-fused by its exact tail."""
-    rng = np.random.default_rng(6)
-    cfg = V.VolumeConfig(voxel_size=0.01, mu=0.06, stream_radius=6.0, hash_buckets=1 << 16)
-    old = S.SPose(S.rot_z(0.2) @ S.rot_y(0.05), [0.1, 0.05, 0.2])
-    new = S.SPose(S.rot_z(0.21) @ S.rot_y(0.06), [0.11, 0.04, 0.21])
-    f0 = _vga_frame(rng)
-    store = V.TwoTierStore(block_capacity=1 << 15)
-    ref = O.OracleStore(cfg.voxel_size, cfg.mu, cfg.stream_radius)
-    V.stream(store, old.translation, cfg)
-    ref.stream(old.translation)
-    V.integrate(store, f0, old, cfg)
-    ref.integrate(f0, old)
-    keys, d, w, c = ref.export()
-    coords = O.keys_to_coords(keys)
-    for j in rng.choice(len(coords), size=min(40, len(coords)), replace=False):
-        b = ref.find(coords[j])
-        vox = rng.choice(512, size=64, replace=False)
-        b.c[vox, 1] = 1e305
-        store.put_block(coords[j], b.d.copy(), b.w.copy(), b.c.copy())
-    ents = [S.Entry(f0, old.copy(), new.copy())]
-    rents = [S.Entry(f0, old.copy(), new.copy())]
-    assert V.correct_entries(store, ents, cfg) == 1
-    ref.correct_entries(rents)
-    assert_same_state(store, ref)
-
-
 @pytest.mark.parametrize("vs", [0.01, 0.005, 0.004])
 def test_footprint_far_from_origin_matches_oracle(V, vs):
     """The footprint kernel skips samples whose affine block estimate is
