@@ -298,6 +298,17 @@ enum { RF_DW_MASK = 1, RF_DW_MASK_ONLY = 2 };
 rf_status rf_depth_weight(const double *depth, int32_t width, int32_t height,
                           double fx, double fy, double cx, double cy,
                           double delta_disc, int32_t flags, double *w_map, void *stream);
+/* normal_map (keyframe_fusion.py:142-188): normals[h][w][3], zero at the
+ * border and next to invalid depth. */
+rf_status rf_normal_map(const double *depth, int32_t width, int32_t height,
+                        double fx, double fy, double cx, double cy,
+                        double *normals, void *stream);
+/* depth_sample_weight(depth, intr, normals) (keyframe_fusion.py:191-208)
+ * with caller-supplied normals[h][w][3]. */
+rf_status rf_depth_sample_weight_normals(const double *depth, const double *normals,
+                                         int32_t width, int32_t height, double fx,
+                                         double fy, double cx, double cy, double *w,
+                                         void *stream);
 /* fuse_depth's warp + np.add.at scatter + Eq. 1 merge (keyframe_fusion.py:
  * 247-276): rel = compose(inverse(kf.pose), frame.pose).  Deterministic:
  * contributions to a keyframe pixel are summed in source-pixel order. */
@@ -332,7 +343,9 @@ typedef struct rf_member_view {
 } rf_member_view;
 
 /* fuse_color (keyframe_fusion.py:377-460): per-channel blur-weighted
- * median over <= 64 members; color_valid[h][w] is 0/1. */
+ * median over any number of members (<= 64: one pass with the samples in
+ * registers / local memory; more: global-scratch pass in pixel chunks);
+ * color_valid[h][w] is 0/1. */
 rf_status rf_fuse_color(const double *kf_depth, const double *kf_weight,
                         int32_t width, int32_t height, double fx, double fy,
                         double cx, double cy, int32_t n_members,

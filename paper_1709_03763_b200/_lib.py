@@ -198,6 +198,10 @@ SIGNATURES = {
                       + [ctypes.c_int32, c_int32_p]),
     "rf_depth_weight": (_S, [_vp, ctypes.c_int32, ctypes.c_int32] + [ctypes.c_double] * 5
                         + [ctypes.c_int32, _vp, _vp]),
+    "rf_normal_map": (_S, [_vp, ctypes.c_int32, ctypes.c_int32] + [ctypes.c_double] * 4
+                      + [_vp, _vp]),
+    "rf_depth_sample_weight_normals": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32]
+                                       + [ctypes.c_double] * 4 + [_vp, _vp]),
     "rf_fuse_depth": (_S, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32]
                       + [ctypes.c_double] * 4 + [ctypes.POINTER(RfPose), ctypes.c_int32, _vp]),
     "rf_unsharp_mask": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_double_p,

@@ -58,21 +58,17 @@ __device__ __forceinline__ void transform(const rf_pose& T, double p0, double p1
 // ---------------------------------------------------------------------------
 // depth sample weight w_z = cos(theta) / Z^2 with the discontinuity mask
 
-// flags: RF_DW_MASK applies the discontinuity mask to w (fuse_depth's
-// w_map); RF_DW_MASK_ONLY writes the mask itself as 1.0 / 0.0.
-__global__ void k_depth_weight(const double* __restrict__ depth, Intr in, double delta_disc,
-                               int flags, double* __restrict__ w_out) {
-  const int u = blockIdx.x * blockDim.x + threadIdx.x;
-  const int v = blockIdx.y * blockDim.y + threadIdx.y;
-  if (u >= in.w || v >= in.h) return;
+// normal_map (:142-188) at one pixel: central differences of unprojected
+// neighbours; borders and pixels with an invalid neighbour get 0.
+__device__ __forceinline__ void normal_at(const double* __restrict__ depth, const Intr& in, int u,
+                                          int v, double& n0, double& n1, double& n2) {
   const int W = in.w, H = in.h;
   auto D = [&](int vv, int uu) { return __ldg(&depth[static_cast<size_t>(vv) * W + uu]); };
   auto dx = [&](int uu) { return (static_cast<double>(uu) - in.cx) / in.fx; };  // ray_grid
   auto dy = [&](int vv) { return (static_cast<double>(vv) - in.cy) / in.fy; };
-  const double d = D(v, u);
-  // normal_map (:142-188): central differences of unprojected neighbours
-  double n0 = 0.0, n1 = 0.0, n2 = 0.0;
+  n0 = n1 = n2 = 0.0;
   if (u >= 1 && u <= W - 2 && v >= 1 && v <= H - 2) {
+    const double d = D(v, u);
     const double dr = D(v, u + 1), dl = D(v, u - 1), dd = D(v + 1, u), du = D(v - 1, u);
     const double xr = dx(u + 1), xl = dx(u - 1), xc = dx(u);
     const double yc = dy(v), yd = dy(v + 1), yu = dy(v - 1);
@@ -89,6 +85,50 @@ __global__ void k_depth_weight(const double* __restrict__ depth, Intr in, double
       n2 = c2 / nrm;
     }
   }
+}
+
+__global__ void k_normal_map(const double* __restrict__ depth, Intr in, double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= in.w || v >= in.h) return;
+  double n0, n1, n2;
+  normal_at(depth, in, u, v, n0, n1, n2);
+  double* o = out + 3 * (static_cast<size_t>(v) * in.w + u);
+  o[0] = n0;
+  o[1] = n1;
+  o[2] = n2;
+}
+
+// depth_sample_weight with caller-supplied normals (:191-208)
+__global__ void k_weight_from_normals(const double* __restrict__ depth,
+                                      const double* __restrict__ normals, Intr in,
+                                      double* __restrict__ w_out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= in.w || v >= in.h) return;
+  const size_t i = static_cast<size_t>(v) * in.w + u;
+  const double rx = (static_cast<double>(u) - in.cx) / in.fx;
+  const double ry = (static_cast<double>(v) - in.cy) / in.fy;
+  const double ray_norm = sqrt(rx * rx + ry * ry + 1.0);
+  const double cos_t = (normals[3 * i] * rx + normals[3 * i + 1] * ry + normals[3 * i + 2]) / ray_norm;
+  const double d = depth[i];
+  w_out[i] = (d > 0 && isfinite(d) && cos_t > 0) ? cos_t / (d * d) : 0.0;
+}
+
+// flags: RF_DW_MASK applies the discontinuity mask to w (fuse_depth's
+// w_map); RF_DW_MASK_ONLY writes the mask itself as 1.0 / 0.0.
+__global__ void k_depth_weight(const double* __restrict__ depth, Intr in, double delta_disc,
+                               int flags, double* __restrict__ w_out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= in.w || v >= in.h) return;
+  const int W = in.w, H = in.h;
+  auto D = [&](int vv, int uu) { return __ldg(&depth[static_cast<size_t>(vv) * W + uu]); };
+  auto dx = [&](int uu) { return (static_cast<double>(uu) - in.cx) / in.fx; };  // ray_grid
+  auto dy = [&](int vv) { return (static_cast<double>(vv) - in.cy) / in.fy; };
+  const double d = D(v, u);
+  double n0, n1, n2;
+  normal_at(depth, in, u, v, n0, n1, n2);
   // depth_sample_weight (:191-208)
   const double rx = dx(u), ry = dy(v);
   const double ray_norm = sqrt(rx * rx + ry * ry + 1.0);
@@ -534,6 +574,98 @@ __global__ void k_fuse_color(const double* __restrict__ kd, const double* __rest
   valid_out[i] = 1;
 }
 
+// fuse_color with more than kMaxMembers members (KF_DIST / KF_OVRLP / KF_DVO
+// keyframes that stay open, or kappa > 64): the same per-pixel semantics with
+// the samples in a global scratch (one row of n_mem per pixel of a chunk) and
+// a stable bottom-up merge sort instead of the insertion sort.  Zero-weight
+// samples take part exactly as in the reference's argsort / cumsum (adding
+// +0.0 never changes the running sum).
+__global__ void k_fuse_color_big(const double* __restrict__ kd, const double* __restrict__ kw,
+                                 Intr in, const MemberDev* __restrict__ tab, int n_mem,
+                                 double delta_occl, int order, int p0, int count,
+                                 double* __restrict__ vals, double* __restrict__ wts,
+                                 int* __restrict__ idx, int* __restrict__ tmp,
+                                 double* __restrict__ color_out,
+                                 unsigned char* __restrict__ valid_out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= count) return;
+  const int i = p0 + t;
+  double* co = color_out + 3 * static_cast<size_t>(i);
+  co[0] = co[1] = co[2] = 0.0;
+  valid_out[i] = 0;
+  if (!(kw[i] > 0.0)) return;
+  double* V = vals + static_cast<size_t>(t) * n_mem * 3;
+  double* Wt = wts + static_cast<size_t>(t) * n_mem;
+  int* I = idx + static_cast<size_t>(t) * n_mem;
+  int* Tm = tmp + static_cast<size_t>(t) * n_mem;
+  const int u = i % in.w, v = i / in.w;
+  const double z = kd[i];
+  const double p0x = ((static_cast<double>(u) - in.cx) / in.fx) * z;
+  const double p1x = ((static_cast<double>(v) - in.cy) / in.fy) * z;
+  for (int m = 0; m < n_mem; ++m) {
+    double c3[3] = {0.0, 0.0, 0.0};
+    double wc = 0.0;
+    const MemberDev& M = tab[m];
+    double q0, q1, q2;
+    transform(M.rel, p0x, p1x, z, order, q0, q1, q2);
+    if (q2 > 0) {
+      const double uu = in.fx * q0 / q2 + in.cx;
+      const double vv = in.fy * q1 / q2 + in.cy;
+      if (uu >= 0 && uu <= in.w - 1 && vv >= 0 && vv <= in.h - 1) {
+        const int un = static_cast<int>(floor(uu + 0.5)), vn = static_cast<int>(floor(vv + 0.5));
+        const size_t q = static_cast<size_t>(vn) * in.w + un;
+        const double zn = M.depth[q];
+        const double w_c = *M.blur * M.w_map[q];
+        if (zn > 0 && fabs(zn - q2) <= delta_occl && w_c > 0) {
+          bilinear(M.color, in.w, in.h, uu, vv, c3);
+          wc = w_c;
+        }
+      }
+    }
+    V[3 * m] = c3[0];
+    V[3 * m + 1] = c3[1];
+    V[3 * m + 2] = c3[2];
+    Wt[m] = wc;
+  }
+  double total = 0.0;
+  for (int m = 0; m < n_mem; ++m) total = total + Wt[m];
+  if (!(total > 0)) return;
+  const double half = total / 2.0;
+  for (int ch = 0; ch < 3; ++ch) {
+    for (int m = 0; m < n_mem; ++m) I[m] = m;
+    // stable bottom-up merge sort of I by V[.][ch]
+    int* src = I;
+    int* dst = Tm;
+    for (int width = 1; width < n_mem; width *= 2) {
+      for (int lo = 0; lo < n_mem; lo += 2 * width) {
+        const int mid = min(lo + width, n_mem), hi = min(lo + 2 * width, n_mem);
+        int a = lo, b = mid, o = lo;
+        while (a < mid && b < hi) {
+          // take from the right run only when strictly smaller: stable
+          if (V[3 * src[b] + ch] < V[3 * src[a] + ch]) dst[o++] = src[b++];
+          else dst[o++] = src[a++];
+        }
+        while (a < mid) dst[o++] = src[a++];
+        while (b < hi) dst[o++] = src[b++];
+      }
+      int* sw = src;
+      src = dst;
+      dst = sw;
+    }
+    double cum = 0.0;
+    int pick = 0;
+    for (int a = 0; a < n_mem; ++a) {
+      cum = cum + Wt[src[a]];
+      if (cum >= half) {
+        pick = a;
+        break;
+      }
+    }
+    co[ch] = V[3 * src[pick] + ch];
+  }
+  valid_out[i] = 1;
+}
+
 Intr make_intr(int w, int h, double fx, double fy, double cx, double cy) {
   Intr in;
   in.w = w;
@@ -859,7 +991,7 @@ rf_status rf_fuse_color(const double* kf_depth, const double* kf_weight, int32_t
                         int32_t blas_order, double* kf_color, uint8_t* color_valid,
                         void* stream) {
   if (!kf_depth || !kf_weight || !kf_color || !color_valid || width <= 0 || height <= 0 ||
-      n_members < 0 || n_members > kMaxMembers || (n_members > 0 && !members))
+      n_members < 0 || (n_members > 0 && !members))
     return RF_INVALID_ARG;
   keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -873,13 +1005,59 @@ rf_status rf_fuse_color(const double* kf_depth, const double* kf_weight, int32_t
     host[m].blur = members[m].blur_weight;
     host[m].rel = members[m].rel;
   }
+  const int n = width * height;
+  if (n_members > kMaxMembers) {  // rare: global-scratch path, pixel chunks
+    const Intr in = make_intr(width, height, fx, fy, cx, cy);
+    const size_t per = static_cast<size_t>(n_members) * (4 * sizeof(double) + 2 * sizeof(int));
+    const int chunk = static_cast<int>(std::max<size_t>(
+        1, std::min<size_t>(n, (size_t(256) << 20) / per)));
+    char* scratch = nullptr;
+    MemberDev* d_tab = nullptr;
+    if (cudaMallocAsync(&scratch, per * chunk, s) != cudaSuccess ||
+        cudaMallocAsync(&d_tab, sizeof(MemberDev) * n_members, s) != cudaSuccess)
+      return RF_CAPACITY;
+    cudaMemcpyAsync(d_tab, host.data(), sizeof(MemberDev) * n_members, cudaMemcpyHostToDevice, s);
+    double* vals = reinterpret_cast<double*>(scratch);
+    double* wts = vals + static_cast<size_t>(chunk) * n_members * 3;
+    int* idx = reinterpret_cast<int*>(wts + static_cast<size_t>(chunk) * n_members);
+    int* tmp = idx + static_cast<size_t>(chunk) * n_members;
+    for (int p0 = 0; p0 < n; p0 += chunk) {
+      const int cnt = std::min(chunk, n - p0);
+      k_fuse_color_big<<<(cnt + 127) / 128, 128, 0, s>>>(kf_depth, kf_weight, in, d_tab,
+                                                          n_members, delta_occl, blas_order, p0,
+                                                          cnt, vals, wts, idx, tmp, kf_color,
+                                                          color_valid);
+    }
+    cudaFreeAsync(d_tab, s);
+    cudaFreeAsync(scratch, s);
+    // the pageable table copy above completed before returning (host order)
+    return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+  }
   MemberTable tab{};
   for (int m = 0; m < n_members; ++m) tab.m[m] = host[m];
-  const int n = width * height;
   k_fuse_color<<<(n + 127) / 128, 128, 0, s>>>(kf_depth, kf_weight,
                                                 make_intr(width, height, fx, fy, cx, cy), tab,
                                                 n_members, delta_occl, blas_order, kf_color,
                                                 color_valid);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_normal_map(const double* depth, int32_t width, int32_t height, double fx,
+                        double fy, double cx, double cy, double* normals, void* stream) {
+  if (!depth || !normals || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  const dim3 blk(32, 8), grd((width + 31) / 32, (height + 7) / 8);
+  k_normal_map<<<grd, blk, 0, static_cast<cudaStream_t>(stream)>>>(
+      depth, make_intr(width, height, fx, fy, cx, cy), normals);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+rf_status rf_depth_sample_weight_normals(const double* depth, const double* normals,
+                                         int32_t width, int32_t height, double fx, double fy,
+                                         double cx, double cy, double* w, void* stream) {
+  if (!depth || !normals || !w || width <= 0 || height <= 0) return RF_INVALID_ARG;
+  const dim3 blk(32, 8), grd((width + 31) / 32, (height + 7) / 8);
+  k_weight_from_normals<<<grd, blk, 0, static_cast<cudaStream_t>(stream)>>>(
+      depth, normals, make_intr(width, height, fx, fy, cx, cy), w);
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }
 

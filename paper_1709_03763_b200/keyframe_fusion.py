@@ -223,12 +223,33 @@ def _depth_weight(depth, intr, delta_disc, flags):
     return out
 
 
+def normal_map(depth, intr):
+    """Unit surface normals [h][w][3] from central differences of unprojected
+    points; zero at the border and next to invalid depth (device;
+    keyframe_fusion.py:142-188)."""
+    torch = _torch()
+    d = _plane(depth, (intr.height, intr.width))
+    out = torch.empty((intr.height, intr.width, 3), dtype=torch.float64, device=d.device)
+    _check(L.lib().rf_normal_map(d.data_ptr(), intr.width, intr.height, float(intr.fx),
+                                 float(intr.fy), float(intr.cx), float(intr.cy),
+                                 out.data_ptr(), _stream()), "rf_normal_map")
+    return out
+
+
 def depth_sample_weight(depth, intr, normals=None):
-    """w_z = cos(theta) / Z^2 (device).  ``normals`` is accepted for API
-    compatibility only when None (the device computes them)."""
-    if normals is not None:
-        raise NotImplementedError("explicit normals are not supported on the device path")
-    return _depth_weight(depth, intr, 0.0, 0)
+    """w_z = cos(theta) / Z^2, zero where invalid (device;
+    keyframe_fusion.py:191-208); ``normals`` default to normal_map(depth)."""
+    if normals is None:
+        return _depth_weight(depth, intr, 0.0, 0)
+    torch = _torch()
+    d = _plane(depth, (intr.height, intr.width))
+    n = _plane(normals, (intr.height, intr.width, 3))
+    out = torch.empty_like(d)
+    _check(L.lib().rf_depth_sample_weight_normals(
+        d.data_ptr(), n.data_ptr(), intr.width, intr.height, float(intr.fx), float(intr.fy),
+        float(intr.cx), float(intr.cy), out.data_ptr(), _stream()),
+        "rf_depth_sample_weight_normals")
+    return out
 
 
 def discontinuity_mask(depth, delta_disc=DELTA_DISC):
@@ -351,8 +372,6 @@ def fuse_color(kf, delta_occl=DELTA_OCCL):
     kf.color = torch.zeros((h, w, 3), dtype=torch.float64, device=kf.depth.device)
     valid = torch.zeros((h, w), dtype=torch.uint8, device=kf.depth.device)
     members = [m for m in kf.observations if m.color is not None]
-    if len(members) > 64:
-        raise ValueError("at most 64 colour members per keyframe on the device path")
     views = (L.RfMemberView * max(len(members), 1))()
     for i, m in enumerate(members):
         views[i].depth = m.depth.data_ptr()

@@ -166,3 +166,54 @@ def test_fusion_reference_test_cases(KF):
     assert cv.any() and np.allclose(kf.color.cpu().numpy()[cv], 12.0, atol=1e-9)
     assert KF.weighted_median([9, 5], [1, 1]) == 5
     assert KF.weighted_median([10, 200], [3, 1]) == 10
+
+
+@needs_ref
+def test_normal_map_and_weight_with_normals_bitexact(KF):
+    """normal_map (keyframe_fusion.py:142-188) and depth_sample_weight with
+    caller-supplied normals (:191-208) on the device."""
+    h, w = 120, 160
+    rng = np.random.default_rng(21)
+    intr, rintr = ref_pair(KF, h, w)
+    depth = scene_depth(h, w, intr.fx, intr.cx, intr.cy, rng)
+    depth[5, 7] = np.nan
+    n_ref = REF["KF"].normal_map(depth, rintr)
+    n_got = KF.normal_map(depth, intr).cpu().numpy()
+    assert np.array_equal(n_got, n_ref)
+    normals = rng.normal(size=(h, w, 3))
+    want = REF["KF"].depth_sample_weight(depth, rintr, normals)
+    got = KF.depth_sample_weight(depth, intr, normals).cpu().numpy()
+    assert np.array_equal(got, want)
+    assert np.array_equal(KF.depth_sample_weight(depth, intr).cpu().numpy(),
+                          REF["KF"].depth_sample_weight(depth, rintr))
+
+
+@needs_ref
+def test_fuse_color_more_than_64_members_bitexact(KF):
+    """A keyframe that stays open for 70 frames (the reference has
+    no member limit): the global-scratch median path."""
+    from paper_1709_03763_b200 import geometry as MG
+
+    h, w, n = 48, 64, 70
+    rng = np.random.default_rng(70)
+    intr, rintr = ref_pair(KF, h, w)
+    RG, RK = REF["G"], REF["KF"]
+    rposes = _poses(RG, n, step=0.002)
+    mposes = [MG.Pose(p.rotation, p.translation) for p in rposes]
+    rkf = mkf = None
+    for i in range(n):
+        d = scene_depth(h, w, intr.fx, intr.cx, intr.cy, rng)
+        c = color_img(h, w, rng)
+        if i % 9 == 4:
+            c = np.full_like(c, 100.0)  # ties between members
+        rf = RK.FrameObservation(i + 1, c, d, rposes[i])
+        mf = KF.FrameObservation(i + 1, c, d, mposes[i])
+        if rkf is None:
+            rkf = RK.new_keyframe(rf, rintr)
+            mkf = KF.new_keyframe(mf, intr)
+        RK.fuse_depth(rkf, rf)
+        KF.fuse_depth(mkf, mf)
+    RK.fuse_color(rkf)
+    KF.fuse_color(mkf)
+    assert np.array_equal(mkf.color_valid.cpu().numpy(), rkf.color_valid)
+    assert np.array_equal(mkf.color.cpu().numpy(), rkf.color)
