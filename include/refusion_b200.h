@@ -275,6 +275,27 @@ rf_status rf_route_ipc_open(rf_volume *vol, const void *handles);
 rf_status rf_route(rf_volume *vol, int32_t n, const rf_kf_view *kfs, const rf_pose *poses,
                    const double *centers);
 
+/* ---- cross-shard removal verdicts (hash-sharded volumes) ----
+ * The reference's de-integration is all-or-nothing over the whole footprint
+ * (volume.py:315-338; the window rollback reintegration.py:166-174).  Once
+ * the shards are connected, every removal's check ends with a device-side
+ * exchange: each shard folds its minimum failing block key into every
+ * shard's slot (remote atomicMin over peer memory) and waits for all of
+ * them, so every shard fails at the same op with the same global key and
+ * applies the same rollback.  Calls that de-integrate (rf_deintegrate,
+ * rf_correct_windows) must then be made in lockstep on every shard (the
+ * callers agree on each call's status); a peer that never arrives turns
+ * into RF_CAPACITY after ~60 s instead of a hang. */
+/* allocate this shard's slots (max_ops ops per call); *slots / *bytes
+ * describe the device buffer */
+rf_status rf_shard_sync_setup(rf_volume *vol, int32_t max_ops, void **slots, uint64_t *bytes);
+/* shards of one process: slots[s] = shard s's buffer (device pointers) */
+rf_status rf_shard_sync_connect(rf_volume *vol, void *const *slots);
+/* shards in separate processes: 64-byte cudaIpcMemHandle_t of this buffer,
+ * and open all shards' handles (shard_count x 64 bytes, own entry ignored) */
+rf_status rf_shard_sync_ipc_handle(rf_volume *vol, void *handle);
+rf_status rf_shard_sync_ipc_open(rf_volume *vol, const void *handles);
+
 /* ---- measurement -------------------------------------------------------- */
 rf_status rf_profile_begin(rf_volume *vol);
 rf_status rf_profile_end(rf_volume *vol, rf_profile *out);

@@ -226,6 +226,11 @@ SIGNATURES = {
     "rf_route_ipc_open": (_S, [_vp, _vp]),
     "rf_route": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfKfView), ctypes.POINTER(RfPose),
                       c_double_p]),
+    "rf_shard_sync_setup": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(_vp),
+                                 ctypes.POINTER(ctypes.c_uint64)]),
+    "rf_shard_sync_connect": (_S, [_vp, ctypes.POINTER(_vp)]),
+    "rf_shard_sync_ipc_handle": (_S, [_vp, _vp]),
+    "rf_shard_sync_ipc_open": (_S, [_vp, _vp]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
     "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4

@@ -137,6 +137,14 @@ struct rf_volume {
   bool route_on = false;
   unsigned route_gen = 0;
   int route_nops = 0;  // ops routed by the last rf_route, consumed by the next call
+  // cross-shard removal verdicts (k_shard_sync): this shard's slots, every
+  // shard's (peers opened over IPC are closed on destroy)
+  SyncSlot* sync_own = nullptr;
+  SyncSlot* sync_peer[kMaxShards] = {};
+  bool sync_ipc[kMaxShards] = {};
+  int sync_max_ops = 0;
+  bool sync_on = false;
+  unsigned sync_gen = 0;
   std::string err;
 };
 
@@ -684,6 +692,18 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     }
     p.capture = nullptr;
     launches += 1;
+    if (v->sync_on) {  // the global verdict of this removal (every shard's check)
+      SyncArgs sa{};
+      for (int s = 0; s < v->cfg.shard_count; ++s) sa.peer[s] = v->sync_peer[s];
+      sa.own = v->sync_own;
+      sa.shards = v->cfg.shard_count;
+      sa.parity = static_cast<int>(v->sync_gen & 1);
+      sa.max_ops = v->sync_max_ops;
+      ProfScope ps(v, 3);
+      launch(k_shard_sync, 1, 32, 0, v->stream, sa, op, v->d_ops + op, v->d_ws,
+             60ull * 2000000000ull);  // ~60 s at 2 GHz: a peer that never comes is an error
+      launches += 1;
+    }
     wait_color(v, kf);  // the check read no colour; the removal does
     {
       ProfScope ps(v, 0);
@@ -709,6 +729,19 @@ void op_gc(Batch& b) {
   launch(k_gc, v->n_sms * 8, 256, 0, v->stream, v->T, op, v->d_ws, &v->d_ops[op].n_new,
          v->d_gc_stamp, v->gc_epoch);
   if (v->profiling) v->prof_launches += 1;
+}
+
+// A connected shard's call that may de-integrate: a new sync generation;
+// the previous call's parity is reset for the next call (all peers finished
+// the previous call: the callers agree on every call's status).
+rf_status sync_begin(rf_volume* v, int max_ops) {
+  if (!v->sync_on) return RF_OK;
+  if (max_ops > v->sync_max_ops)
+    return fail(v, RF_INVALID_ARG, "shard sync: more ops in one call than the sync slots hold");
+  ++v->sync_gen;
+  launch(k_sync_reset, 8, 256, 0, v->stream, v->sync_own, v->sync_max_ops,
+         static_cast<int>((v->sync_gen ^ 1u) & 1u));
+  return RF_OK;
 }
 
 struct BatchOutcome {
@@ -926,9 +959,12 @@ rf_status rf_volume_destroy(rf_volume* v) {
     if (sl.consumed) cudaEventDestroy(sl.consumed);
   }
   if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
-  for (int s = 0; s < kMaxShards; ++s)
+  for (int s = 0; s < kMaxShards; ++s) {
     if (v->route_ipc[s]) cudaIpcCloseMemHandle(v->route_peer[s]);
+    if (v->sync_ipc[s]) cudaIpcCloseMemHandle(v->sync_peer[s]);
+  }
   if (v->route_own) cudaFree(v->route_own);
+  if (v->sync_own) cudaFree(v->sync_own);
   delete v;
   return RF_OK;
 }
@@ -1117,6 +1153,65 @@ rf_status rf_route(rf_volume* v, int32_t n, const rf_kf_view* kfs, const rf_pose
   return RF_OK;
 }
 
+// ---- cross-shard removal verdicts (k_shard_sync) ---------------------------
+
+rf_status rf_shard_sync_setup(rf_volume* v, int32_t max_ops, void** slots, uint64_t* bytes) {
+  if (!v || max_ops <= 0 || v->cfg.shard_count < 2 || v->cfg.shard_count > kMaxShards)
+    return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  if (v->sync_own) return fail(v, RF_INVALID_ARG, "rf_shard_sync_setup: already set up");
+  const size_t n = 2 * static_cast<size_t>(max_ops) * sizeof(SyncSlot);
+  void* mem = nullptr;
+  RF_CUDA_TRY(v, cudaMalloc(&mem, n));
+  v->sync_own = static_cast<SyncSlot*>(mem);
+  v->sync_max_ops = max_ops;
+  for (int par = 0; par < 2; ++par)
+    k_sync_reset<<<8, 256, 0, v->stream>>>(v->sync_own, max_ops, par);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+  if (slots) *slots = mem;
+  if (bytes) *bytes = n;
+  return RF_OK;
+}
+
+rf_status rf_shard_sync_connect(rf_volume* v, void* const* slots) {
+  if (!v || !slots || !v->sync_own) return RF_INVALID_ARG;
+  if (slots[v->cfg.shard_rank] != v->sync_own)
+    return fail(v, RF_INVALID_ARG, "rf_shard_sync_connect: own slots mismatch");
+  for (int s = 0; s < v->cfg.shard_count; ++s) {
+    if (!slots[s]) return RF_INVALID_ARG;
+    v->sync_peer[s] = static_cast<SyncSlot*>(slots[s]);
+  }
+  v->sync_on = true;
+  return RF_OK;
+}
+
+rf_status rf_shard_sync_ipc_handle(rf_volume* v, void* handle) {
+  if (!v || !handle || !v->sync_own) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaIpcMemHandle_t h;
+  RF_CUDA_TRY(v, cudaIpcGetMemHandle(&h, v->sync_own));
+  std::memcpy(handle, &h, sizeof(h));
+  return RF_OK;
+}
+
+rf_status rf_shard_sync_ipc_open(rf_volume* v, const void* handles) {
+  if (!v || !handles || !v->sync_own) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  const int G = v->cfg.shard_count;
+  std::vector<void*> ptrs(G, nullptr);
+  for (int s = 0; s < G; ++s) {
+    if (s == v->cfg.shard_rank) {
+      ptrs[s] = v->sync_own;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + s * sizeof(h), sizeof(h));
+    RF_CUDA_TRY(v, cudaIpcOpenMemHandle(&ptrs[s], h, cudaIpcMemLazyEnablePeerAccess));
+    v->sync_ipc[s] = true;
+  }
+  return rf_shard_sync_connect(v, ptrs.data());
+}
+
 rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,
                       int64_t* new_keys_host, int64_t cap, int64_t* n_new) {
   if (!v || !valid_kf(kf) || !pose) return RF_INVALID_ARG;
@@ -1187,6 +1282,8 @@ rf_status rf_deintegrate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose
   Batch b;
   rf_status st = batch_begin(v, b, 1);
   if (st != RF_OK) return st;
+  st = sync_begin(v, 1);
+  if (st != RF_OK) return st;
   op_fuse(b, kf, pose, 1, 0);
   BatchOutcome o;
   st = batch_end(b, o);
@@ -1225,6 +1322,8 @@ rf_status rf_correct_windows(rf_volume* v, int32_t n_windows, const int32_t* siz
   Batch b;
   // per window: stream(old0) + m x (stream, deint) + stream(new0) + m x (stream, int) + gc
   rf_status st = batch_begin(v, b, static_cast<int>(4 * total + 3 * n_windows + 1));
+  if (st != RF_OK) return st;
+  st = sync_begin(v, static_cast<int>(4 * total + 3 * n_windows + 1));
   if (st != RF_OK) return st;
   // each window is reintegration._correct_entries (reintegration.py:156-181)
   long long base = 0;

@@ -766,6 +766,17 @@ def _route_cap(shards, image=(640, 480)):
     return -(-tiles // shards) * 512 + 4096
 
 
+# ops of one native call a connected shard's verdict slots cover: a batch of
+# w windows / n entries has 4n + 3w + 1 ops (rf_correct_windows)
+_SYNC_OPS = 7 * MAX_WINDOW_ENTRIES + 8
+
+
+def _sync_setup(store):
+    slots, nbytes = ctypes.c_void_p(), ctypes.c_uint64()
+    store._call("rf_shard_sync_setup", _SYNC_OPS, ctypes.byref(slots), ctypes.byref(nbytes))
+    return slots.value
+
+
 def _route_setup(store, max_ops, cap_keys):
     inbox, nbytes = ctypes.c_void_p(), ctypes.c_uint64()
     store._call("rf_route_setup", int(max_ops), int(cap_keys), ctypes.byref(inbox),
@@ -786,6 +797,12 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
         raise ValueError("connect_shards needs one store per shard rank 0..G-1")
     for s in stores:
         s._bind(cfg)
+    # cross-shard removal verdicts (k_shard_sync): every de-integration fails
+    # on all shards at the same op with the same key, as one volume would
+    slots = {s.shard_rank: _sync_setup(s) for s in stores}
+    sarr = (ctypes.c_void_p * G)(*[slots[r] for r in range(G)])
+    for s in stores:
+        s._call("rf_shard_sync_connect", sarr)
     group = _ThreadGroup(G, timeout)
     if not route:  # replicated sampling: only the status agreement
         for s in stores:
@@ -819,14 +836,20 @@ def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640
         dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
         return int(t.item())
 
+    G = store.shard_count
+    store._bind(cfg)
+    # cross-shard removal verdicts: slots exchanged once as CUDA IPC handles
+    _sync_setup(store)
+    h = (ctypes.c_char * 64)()
+    store._call("rf_shard_sync_ipc_handle", h)
+    handles = [None] * G
+    dist.all_gather_object(handles, bytes(h), group=group)
+    store._call("rf_shard_sync_ipc_open", ctypes.c_char_p(b"".join(handles)))
     if not route:
-        store._bind(cfg)
         store._router = _ShardRouter(max_ops, lambda: dist.barrier(group=group), agree,
                                      routed=False)
         return
-    G = store.shard_count
     cap = cap_keys or _route_cap(G, image)
-    store._bind(cfg)
     _route_setup(store, max_ops, cap)
     h = (ctypes.c_char * 64)()
     store._call("rf_route_ipc_handle", h)
