@@ -111,12 +111,50 @@ class ClockSampler:
 
 
 def kf_poses(n_kf):
+    """Ground-truth frame poses (kappa per keyframe), the keyframes' ground
+    truth (their first frame) and drifted keyframe pose estimates."""
     from paper_1709_03763_b200 import synth as SY
 
     gt = SY.corridor_trajectory(n_kf * KAPPA)
     gt_kf = [gt[i * KAPPA] for i in range(n_kf)]
     drifted = SY.drift_poses(gt_kf, DRIFT_T, DRIFT_R, seed=1)
-    return gt_kf, drifted
+    return gt, gt_kf, drifted
+
+
+def frame_seed(j):
+    return 1000 + j
+
+
+def build_keyframes(n_kf, gt, drifted, device=0, rank=0, world=1):
+    """The workload's keyframes: KAPPA frames each, rendered at ground truth
+    and fused on the device at their drifted estimates (new_keyframe /
+    fuse_depth / fuse_color) on rank 0, broadcast to every shard."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1709_03763_b200 import synth as SY
+
+    dev = torch.device(f"cuda:{device}")
+    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=device)
+    keyframes = []
+    for k in range(n_kf):
+        if rank == 0:
+            k0 = k * KAPPA
+            kf = SY.fused_keyframe(rend, gt[k0:k0 + KAPPA],
+                                   SY.burst_poses(gt, k, drifted[k], KAPPA),
+                                   [frame_seed(k0 + j) for j in range(KAPPA)], first_index=k0 + 1)
+        else:
+            kf = SY.DeviceKeyframe(SY.DEFAULT_INTRINSICS, drifted[k],
+                                   torch.empty((H, W), dtype=torch.float64, device=dev),
+                                   torch.empty((H, W), dtype=torch.float64, device=dev),
+                                   torch.empty((H, W, 3), dtype=torch.float64, device=dev))
+        if world > 1:
+            for t in (kf.depth, kf.weight, kf.color):
+                dist.broadcast(t, src=0)
+        kf.pose = drifted[k]
+        keyframes.append(kf)
+    torch.cuda.synchronize()
+    return keyframes
 
 
 def make_events(n_anchors, n_events, seed=11):
@@ -187,24 +225,13 @@ def run_b200(args):
     dev = torch.device(f"cuda:{local}")
 
     n_kf = args.keyframes
-    gt_kf, drifted = kf_poses(n_kf)
-    # keyframes: rendered at ground truth on rank 0, broadcast to every shard
-    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=local)
-    keyframes = []
-    for k in range(n_kf):
-        if rank == 0:
-            kf = SY.render_keyframe(rend, gt_kf[k], seed=1000 + k, kappa=KAPPA)
-        else:
-            kf = SY.DeviceKeyframe(SY.DEFAULT_INTRINSICS, gt_kf[k],
-                                   torch.empty((H, W), dtype=torch.float64, device=dev),
-                                   torch.empty((H, W), dtype=torch.float64, device=dev),
-                                   torch.empty((H, W, 3), dtype=torch.float64, device=dev))
-        if world > 1:
-            for t in (kf.depth, kf.weight, kf.color):
-                dist.broadcast(t, src=0)
-        kf.pose = drifted[k]
-        keyframes.append(kf)
-    torch.cuda.synchronize()
+    gt, gt_kf, drifted = kf_poses(n_kf)
+    # keyframes: KAPPA frames each rendered at ground truth and fused on the
+    # device at their drifted estimates (new_keyframe / fuse_depth /
+    # fuse_color) on rank 0, broadcast to every shard
+    t_fuse = time.time()
+    keyframes = build_keyframes(n_kf, gt, drifted, local, rank, world)
+    fuse_s = time.time() - t_fuse
 
     cfg = V.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS, hash_buckets=1 << 21)
     cap = int(os.environ.get("RF_BENCH_BLOCKS", str(2_600_000 // world + 200_000)))
@@ -219,9 +246,10 @@ def run_b200(args):
     scen = Scenario(R, G, SY, gt_kf, drifted, keyframes,
                     make_events((n_kf + EVENT_EVERY_KF - 1) // EVENT_EVERY_KF, n_events))
     t0 = time.time()
+    build_vox = []
     for kf, pose in zip(keyframes, drifted):   # pipeline.close_keyframe, untimed
         V.stream(store, pose.translation, cfg)
-        V.integrate(store, kf, pose, cfg)
+        build_vox.append(V.integrate(store, kf, pose, cfg).voxels_updated)
     torch.cuda.synchronize()
     build_s = time.time() - t0
     n_blocks = store.block_count()
@@ -274,12 +302,13 @@ def run_b200(args):
     prof_steps = max(2, min(args.steps, 5))
     lib.rf_profile_begin(vol)
     prof_ms = 0.0
+    prof_corrected = 0
     for _ in range(prof_steps):
         picks, nxt = prepare()
         flush.zero_()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(stream)
-        R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+        prof_corrected += R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
         b.record(stream)
         b.synchronize()
         prof_ms += a.elapsed_time(b)
@@ -338,13 +367,20 @@ def run_b200(args):
     step_ms = total_ms / args.steps
     alg_bytes = 80.0 * prof.voxels_updated + 40.0 * prof.pixels
     achieved = alg_bytes / (prof.fuse_ms / 1e3) / 1e9 if prof.fuse_ms > 0 else None
-    traffic = None
+    # DRAM traffic of the same kernel from one ncu --set full capture
+    # (tools/prof_workload.py: the bench's keyframes and corrections), with
+    # the algorithmic bytes of the SAME captured launches beside it
+    traffic = t_alg = None
     tpath = os.path.join(REPO, "profiles", "fuse_traffic.json")
     if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("bytes_per_launch")
+        tj = json.load(open(tpath))
+        traffic, t_alg = tj.get("bytes_per_launch"), tj.get("alg_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-            "traffic": traffic, "kernel": "k_fuse<kIntegrate|kApplyRemove>",
+            "traffic": traffic, "traffic_alg_bytes_per_launch": t_alg,
+            "traffic_over_alg": (traffic / t_alg) if traffic and t_alg else None,
+            "traffic_source": "profiles/fuse_traffic.json (ncu capture of tools/prof_workload.py)",
+            "kernel": "k_fuse<kIntegrate|kApplyRemove>",
             "launches": int(prof.fuse_launches),
             "avg_launch_us": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1),
             "alg_bytes_per_launch": alg_bytes / max(prof.fuse_launches, 1),
@@ -375,11 +411,17 @@ def run_b200(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (GPU sphere-traced analytic corridor, sigma0 z^2 depth noise)",
+        "data": "synthetic (GPU sphere-traced analytic corridor, sigma0 z^2 depth noise; "
+                "keyframes fused on the device from 5 rendered frames each)",
         "config": {"workload": WORKLOAD, "keyframes": n_kf, "m": args.m,
                    "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS,
                    "hash_buckets": cfg.hash_buckets, "blocks_resident": n_blocks,
                    "block_capacity": cap, "volume_build_s": round(build_s, 2),
+                   "frames_fused": n_kf * KAPPA, "fusion_s": round(fuse_s, 2),
+                   "voxels_updated_per_integrate": {
+                       "build_mean": statistics.mean(build_vox),
+                       "build_first3": build_vox[:3],
+                       "corrections_mean": prof.voxels_updated / max(2 * prof_corrected, 1)},
                    "parallelism": (f"hash-sharded x{world}" + (", routed footprints" if routed else ""))
                    if world > 1 else "single GPU",
                    "l2": "flushed between steps (256 MiB write, outside the step events)"},
@@ -428,11 +470,13 @@ class _HostKF:
         self.depth, self.weight, self.color, self.intrinsics = depth, weight, color, intr
 
 
-def _reference_store(RG, RV, kfs_np, drifted, cfg):
+def _reference_store(RG, RV, kfs_np, drifted, cfg, vox=None):
     store = RV.TwoTierStore()
     for kf, p in zip(kfs_np, drifted):
         RV.stream(store, p.translation, cfg)
-        RV.integrate(store, kf, _ref_pose(RG, p), cfg)
+        rec = RV.integrate(store, kf, _ref_pose(RG, p), cfg)
+        if vox is not None:
+            vox.append(rec.voxels_updated)
     return store
 
 
@@ -445,8 +489,11 @@ def cpu_baseline_from(keyframes, drifted, gt_kf):
     kfs = [_HostKF(k.depth.cpu().numpy(), k.weight.cpu().numpy(), k.color.cpu().numpy(), intr)
            for k in keyframes]
     cfg = RV.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS)
-    store = _reference_store(RG, RV, kfs, drifted, cfg)
-    return _time_reference_corrections(RG, RR, RV, store, kfs, drifted, gt_kf, cfg, n=2)
+    vox = []
+    store = _reference_store(RG, RV, kfs, drifted, cfg, vox)
+    out = _time_reference_corrections(RG, RR, RV, store, kfs, drifted, gt_kf, cfg, n=2)
+    out["voxels_updated_per_integrate"] = vox
+    return out
 
 
 def _time_reference_corrections(RG, RR, RV, store, kfs, drifted, gt_kf, cfg, n):
@@ -476,12 +523,13 @@ def run_reference(args):
     import numpy as np
 
     RG, RR, RV = _import_reference()
+    from refusion import keyframe_fusion as RF
     from refusion import synth as RS
 
     from paper_1709_03763_b200 import synth as SY  # host-only pose helpers / scene spec
 
     n_kf = 3
-    gt_kf, drifted = kf_poses(args.keyframes)
+    gt, gt_kf, drifted = kf_poses(args.keyframes)
     gt_kf, drifted = gt_kf[:n_kf], drifted[:n_kf]
     prims = []
     for p in SY.corridor_scene():
@@ -494,15 +542,28 @@ def run_reference(args):
     scene = RS.AnalyticScene(prims)
     intr = RS.DEFAULT_INTRINSICS
     kfs = []
+    # the same keyframes as the B200 arm's first three: KAPPA frames each,
+    # rendered at ground truth by the reference renderer and fused at their
+    # drifted estimates by the reference's own keyframe fusion
     for k in range(n_kf):
-        gp = _ref_pose(RG, gt_kf[k])
-        depth = RS.add_noise(RS.render_depth(scene, gp, intr, z_max=5.0), seed=(1, 7, k),
-                             sigma0=0.0015)
-        color = RS.render_color(scene, gp, intr, depth)
-        weight = np.where(depth > 0, KAPPA / np.maximum(depth * depth, 1e-12), 0.0)
-        kfs.append(_HostKF(depth, weight, color, intr))
+        k0 = k * KAPPA
+        est = SY.burst_poses(gt, k, drifted[k], KAPPA)
+        kf = None
+        for j in range(KAPPA):
+            gp = _ref_pose(RG, gt[k0 + j])
+            depth = RS.add_noise(RS.render_depth(scene, gp, intr, z_max=5.0), seed=(1, 7, k0 + j),
+                                 sigma0=0.0015)
+            color = RS.render_color(scene, gp, intr, depth)
+            obs = RF.FrameObservation(index=k0 + j + 1, color=color, depth=depth,
+                                      pose=_ref_pose(RG, est[j]))
+            if kf is None:
+                kf = RF.new_keyframe(obs, intr)
+            RF.fuse_depth(kf, obs)
+        RF.fuse_color(kf)
+        kfs.append(_HostKF(kf.depth, kf.weight, kf.color, intr))
     cfg = RV.VolumeConfig(voxel_size=VOXEL, mu=MU, stream_radius=RADIUS)
-    store = _reference_store(RG, RV, kfs, drifted, cfg)
+    vox = []
+    store = _reference_store(RG, RV, kfs, drifted, cfg, vox)
     times = []
     for s in range(args.warmup + args.steps):
         # each step: one correction re-integrating one keyframe (bounded sample)
@@ -527,9 +588,12 @@ def run_reference(args):
         "value": value, "unit": "keyframes/s", "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference synth.py renderer, same corridor scene and poses)",
+        "data": "synthetic (reference synth.py renderer + reference keyframe fusion, same "
+                "corridor scene, frames and poses)",
         "config": {"workload": WORKLOAD, "sample": "each step = one single-keyframe "
-                   "correction (correct_topk, m=1) on a 3-keyframe corridor volume",
+                   "correction (correct_topk, m=1) on a volume of the workload's first 3 "
+                   "keyframes (each fused from 5 rendered frames)",
+                   "voxels_updated_per_integrate": vox,
                    "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS},
         "cpu_baseline": {"value": value, "unit": "keyframes/s", "cores": 1,
                          "threads_available": os.cpu_count(), "kind": "reference",

@@ -296,6 +296,14 @@ rf_status rf_shard_sync_connect(rf_volume *vol, void *const *slots);
 rf_status rf_shard_sync_ipc_handle(rf_volume *vol, void *handle);
 rf_status rf_shard_sync_ipc_open(rf_volume *vol, const void *handles);
 
+/* Pre-allocate what a call may otherwise allocate lazily: op records for
+ * max_ops ops, the host-keyframe staging ring for width x height keyframes
+ * (colour included) and the footprint memo arena.  Connected shards call it
+ * before their lockstep phase: growing a buffer synchronises the device,
+ * which must not happen while a peer on the same device waits in
+ * k_shard_sync (shards emulated in one process). */
+rf_status rf_reserve(rf_volume *vol, int32_t width, int32_t height, int32_t max_ops);
+
 /* ---- measurement -------------------------------------------------------- */
 rf_status rf_profile_begin(rf_volume *vol);
 rf_status rf_profile_end(rf_volume *vol, rf_profile *out);
@@ -337,6 +345,19 @@ rf_status rf_fuse_depth(double *kf_depth, double *kf_weight, const double *frame
                         const double *w_map, int32_t width, int32_t height,
                         double fx, double fy, double cx, double cy,
                         const rf_pose *rel, int32_t blas_order, void *stream);
+/* One frame of fuse_depth (keyframe_fusion.py:238-296) in one call: the
+ * member's weight map (depth_sample_weight masked by discontinuity_mask,
+ * delta_disc) into w_map, its depth copy into depth_copy, the warp +
+ * np.add.at scatter + Eq. 1 merge into the keyframe planes (as
+ * rf_fuse_depth), and -- frame_color non-null -- the colour prep of
+ * rf_color_prep into member_color / blur_weight.  Replaces the reference's
+ * per-frame sequence of whole-image numpy passes (:245-296). */
+rf_status rf_fuse_frame(double *kf_depth, double *kf_weight, const double *frame_depth,
+                        const double *frame_color, int32_t width, int32_t height,
+                        double fx, double fy, double cx, double cy, const rf_pose *rel,
+                        int32_t blas_order, double delta_disc, const double *gauss_weights,
+                        int32_t radius, double gain, double *w_map, double *depth_copy,
+                        double *member_color, double *blur_weight, void *stream);
 /* unsharp_mask (keyframe_fusion.py:335-346) of an [h][w][channels] image:
  * scipy gaussian_filter (mode 'nearest', gauss_weights[2*radius+1] =
  * _gaussian_kernel1d) per channel, then clip(img + gain*(img - low), 0, 255). */

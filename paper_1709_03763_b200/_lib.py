@@ -204,6 +204,10 @@ SIGNATURES = {
                                        + [ctypes.c_double] * 4 + [_vp, _vp]),
     "rf_fuse_depth": (_S, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32]
                       + [ctypes.c_double] * 4 + [ctypes.POINTER(RfPose), ctypes.c_int32, _vp]),
+    "rf_fuse_frame": (_S, [_vp, _vp, _vp, _vp, ctypes.c_int32, ctypes.c_int32]
+                      + [ctypes.c_double] * 4 + [ctypes.POINTER(RfPose), ctypes.c_int32,
+                                                 ctypes.c_double, c_double_p, ctypes.c_int32,
+                                                 ctypes.c_double, _vp, _vp, _vp, _vp, _vp]),
     "rf_unsharp_mask": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, c_double_p,
                              ctypes.c_int32, ctypes.c_double, _vp, _vp]),
     "rf_grayscale": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, _vp, _vp]),
@@ -231,6 +235,7 @@ SIGNATURES = {
     "rf_shard_sync_connect": (_S, [_vp, ctypes.POINTER(_vp)]),
     "rf_shard_sync_ipc_handle": (_S, [_vp, _vp]),
     "rf_shard_sync_ipc_open": (_S, [_vp, _vp]),
+    "rf_reserve": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
     "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4

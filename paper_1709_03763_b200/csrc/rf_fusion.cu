@@ -15,6 +15,7 @@
 // geometry.transform (p @ R.T + t through BLAS): its multiply-add order is
 // a parameter (rf_blas_order), calibrated on the host at start-up
 // (keyframe_fusion.detect_blas_order).
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -189,6 +190,68 @@ __global__ void k_warp(const double* __restrict__ depth, const double* __restric
   target[i] = t;
 }
 
+// fuse_depth's per-pixel front half in one pass (:245-269): the member's
+// weight map w = depth_sample_weight masked by discontinuity_mask (the
+// k_depth_weight arithmetic), the member's depth copy, then the warp of a
+// weighted pixel into the keyframe (k_warp) -- target pixel, its two
+// summands and the per-target count.
+__global__ void k_dw_warp(const double* __restrict__ depth, Intr in, double delta_disc,
+                          rf_pose rel, int order, double* __restrict__ w_map,
+                          double* __restrict__ depth_copy, int* __restrict__ target,
+                          double* __restrict__ val_wz, double* __restrict__ val_w,
+                          int* __restrict__ counts) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= in.w || v >= in.h) return;
+  const int W = in.w, H = in.h;
+  const size_t i = static_cast<size_t>(v) * W + u;
+  auto D = [&](int vv, int uu) { return __ldg(&depth[static_cast<size_t>(vv) * W + uu]); };
+  const double d = D(v, u);
+  double n0, n1, n2;
+  normal_at(depth, in, u, v, n0, n1, n2);
+  const double rx = (static_cast<double>(u) - in.cx) / in.fx;
+  const double ry = (static_cast<double>(v) - in.cy) / in.fy;
+  const double ray_norm = sqrt(rx * rx + ry * ry + 1.0);
+  const double cos_t = (n0 * rx + n1 * ry + n2) / ray_norm;
+  double w = 0.0;
+  if (d > 0 && isfinite(d) && cos_t > 0) w = cos_t / (d * d);
+  bool masked = !(d > 0);
+  if (!masked) {
+    for (int sv = -1; sv <= 1 && !masked; ++sv)
+      for (int su = -1; su <= 1; ++su) {
+        if (sv == 0 && su == 0) continue;
+        const int nv = v + sv, nu = u + su;
+        if (nv < 0 || nv >= H || nu < 0 || nu >= W) continue;
+        const double nb = D(nv, nu);
+        if (!(nb > 0) || fabs(d - nb) > delta_disc) {
+          masked = true;
+          break;
+        }
+      }
+  }
+  if (masked) w = 0.0;
+  w_map[i] = w;
+  depth_copy[i] = d;
+  int t = -1;
+  if (w > 0.0) {  // k_warp
+    const double p0 = ((static_cast<double>(u) - in.cx) / in.fx) * d;
+    const double p1 = ((static_cast<double>(v) - in.cy) / in.fy) * d;
+    double q0, q1, q2;
+    transform(rel, p0, p1, d, order, q0, q1, q2);
+    if (q2 > 0) {
+      const double uf = floor(in.fx * q0 / q2 + in.cx + 0.5);
+      const double vf = floor(in.fy * q1 / q2 + in.cy + 0.5);
+      if (uf >= 0 && uf < in.w && vf >= 0 && vf < in.h) {
+        t = static_cast<int>(vf) * in.w + static_cast<int>(uf);
+        val_wz[i] = w * q2;
+        val_w[i] = w;
+        atomicAdd(&counts[t], 1);
+      }
+    }
+  }
+  target[i] = t;
+}
+
 // exclusive scan of n ints: per-CTA sums, a single-CTA scan of those, apply
 constexpr int kScanBlock = 1024;
 
@@ -317,6 +380,20 @@ __global__ void k_gauss_rows(const double* __restrict__ img, int W, int H, int C
   for (int ch = 0; ch < C; ++ch)
     out[(static_cast<size_t>(v) * W + u) * C + ch] =
         corr_sym(img + static_cast<size_t>(u) * C + ch, W * C, H, v, g.w, g.r);
+}
+
+// grayscale (:303-307) fused into the first (vertical) Gaussian pass, which
+// reads the same frame colour
+__global__ void k_gauss_rows_gray(const double* __restrict__ img, int W, int H, GaussW g,
+                                  double* __restrict__ out, double* __restrict__ gray) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= W || v >= H) return;
+  const size_t px = static_cast<size_t>(v) * W + u;
+  for (int ch = 0; ch < 3; ++ch)
+    out[px * 3 + ch] = corr_sym(img + static_cast<size_t>(u) * 3 + ch, W * 3, H, v, g.w, g.r);
+  const double* c = img + 3 * px;
+  gray[px] = 0.299 * c[0] + 0.587 * c[1] + 0.114 * c[2];
 }
 
 // pass along axis 1, then unsharp: clip(img + gain * (img - low), 0, 255)
@@ -826,6 +903,50 @@ void keep_pool() {
   done.push_back(dev);
 }
 
+// blurriness (:310-332) of a gray image into caller scratch: b (n),
+// buf (4n: d_f and v per axis), sums (4 doubles).
+rf_status blurriness_core(const double* gray, int width, int height, double* b, double* buf,
+                          double* sums, double* blur_weight, cudaStream_t s) {
+  const long long n = static_cast<long long>(width) * height;
+  // per axis: d_f and v = max(0, d_f - d_b), then the four pairwise sums at once
+  const double* arr[4];
+  long long cnt[4];
+  double* outs[4];
+  int axes = 0;
+  for (int axis = 0; axis < 2; ++axis) {
+    const int len = axis == 0 ? height : width;
+    if (len < 2) continue;
+    const int lines = axis == 0 ? width : height;
+    double* d_f = buf + 2 * axes * n;
+    double* vv = d_f + n;
+    if (len <= kBlurMaxLen) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_blur_lines_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(sizeof(double) * 2 * kBlurMaxLen * kBlurWarps));
+        attr = true;
+      }
+      k_blur_lines_smem<<<(lines + kBlurWarps - 1) / kBlurWarps, 32 * kBlurWarps,
+                          sizeof(double) * 2 * len * kBlurWarps, s>>>(gray, width, height, axis,
+                                                                     9, b, d_f, vv);
+    } else {
+      k_blur_lines<<<(lines + 63) / 64, 64, 0, s>>>(gray, width, height, axis, 9, b, d_f, vv);
+    }
+    const long long m = axis == 0 ? static_cast<long long>(height - 1) * width
+                                  : static_cast<long long>(height) * (width - 1);
+    arr[2 * axes] = d_f;
+    arr[2 * axes + 1] = vv;
+    cnt[2 * axes] = cnt[2 * axes + 1] = m;
+    outs[2 * axes] = sums + 2 * axes;
+    outs[2 * axes + 1] = sums + 2 * axes + 1;
+    ++axes;
+  }
+  rf_status st = RF_OK;
+  if (axes > 0 && pairwise_sums(2 * axes, arr, cnt, outs, s) != RF_OK) st = RF_CUDA;
+  k_blur_finish<<<1, 1, 0, s>>>(sums, axes, blur_weight);
+  return st;
+}
+
 }  // namespace
 
 extern "C" {
@@ -881,6 +1002,71 @@ rf_status rf_fuse_depth(double* kf_depth, double* kf_weight, const double* frame
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }
 
+rf_status rf_fuse_frame(double* kf_depth, double* kf_weight, const double* frame_depth,
+                        const double* frame_color, int32_t width, int32_t height, double fx,
+                        double fy, double cx, double cy, const rf_pose* rel, int32_t blas_order,
+                        double delta_disc, const double* gauss_weights, int32_t radius,
+                        double gain, double* w_map, double* depth_copy, double* member_color,
+                        double* blur_weight, void* stream) {
+  if (!kf_depth || !kf_weight || !frame_depth || !rel || !w_map || !depth_copy ||
+      width <= 0 || height <= 0 || static_cast<long long>(width) * height >= (1LL << 30))
+    return RF_INVALID_ARG;
+  if (frame_color && (!member_color || !blur_weight || !gauss_weights || radius < 0 ||
+                      radius > 15))
+    return RF_INVALID_ARG;
+  keep_pool();
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int n = width * height;
+  // one scratch allocation: ints [target | counts | cursor | offsets | slots],
+  // doubles [val_wz | val_w | gray | gauss tmp (3n) | blur b | blur buf (4n) | sums]
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<const int*>(nullptr),
+                                static_cast<int*>(nullptr), n, s);
+  const size_t ints = 5 * static_cast<size_t>(n);
+  const size_t dbl = (frame_color ? 11 : 2) * static_cast<size_t>(n) + 4;
+  const size_t off_d = (sizeof(int) * ints + 255) & ~size_t(255);
+  const size_t off_scan = (off_d + sizeof(double) * dbl + 255) & ~size_t(255);
+  char* mem = nullptr;
+  if (cudaMallocAsync(&mem, off_scan + scan_bytes, s) != cudaSuccess) return RF_CUDA;
+  int* target = reinterpret_cast<int*>(mem);
+  int* counts = target + n;
+  int* cursor = counts + n;
+  int* offsets = cursor + n;
+  int* slots = offsets + n;
+  double* vwz = reinterpret_cast<double*>(mem + off_d);
+  double* vw = vwz + n;
+  const Intr in = make_intr(width, height, fx, fy, cx, cy);
+  cudaMemsetAsync(counts, 0, sizeof(int) * 2 * n, s);  // counts + cursor
+  const dim3 blk(32, 8), grd((width + 31) / 32, (height + 7) / 8);
+  k_dw_warp<<<grd, blk, 0, s>>>(frame_depth, in, delta_disc, *rel, blas_order, w_map, depth_copy,
+                                target, vwz, vw, counts);
+  cub::DeviceScan::ExclusiveSum(mem + off_scan, scan_bytes, counts, offsets, n, s);
+  k_scatter<<<(n + 255) / 256, 256, 0, s>>>(target, n, offsets, cursor, slots);
+  k_merge<<<(n + 255) / 256, 256, 0, s>>>(kf_depth, kf_weight, n, counts, offsets, slots, vwz, vw);
+  rf_status st = RF_OK;
+  if (frame_color) {  // colour prep (:278-281): unsharp mask + blurriness of grayscale
+    double* gray = vw + n;
+    double* gtmp = gray + n;
+    double* bb = gtmp + 3 * static_cast<size_t>(n);
+    double* bbuf = bb + n;
+    double* sums = bbuf + 4 * static_cast<size_t>(n);
+    GaussW g;
+    g.r = radius;
+    for (int j = 0; j <= radius; ++j) g.w[j] = gauss_weights[radius + j];  // symmetric
+    k_gauss_rows_gray<<<grd, blk, 0, s>>>(frame_color, width, height, g, gtmp, gray);
+    if (gain == 0.0)  // unsharp_mask returns img.copy() (:338-339)
+      cudaMemcpyAsync(member_color, frame_color, sizeof(double) * 3 * n,
+                      cudaMemcpyDeviceToDevice, s);
+    else
+      k_gauss_cols_unsharp<<<grd, blk, 0, s>>>(frame_color, gtmp, width, height, 3, g, gain,
+                                               member_color);
+    st = blurriness_core(gray, width, height, bb, bbuf, sums, blur_weight, s);
+  }
+  cudaFreeAsync(mem, s);
+  if (st != RF_OK) return st;
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
 rf_status rf_unsharp_mask(const double* img, int32_t width, int32_t height, int32_t channels,
                           const double* gauss_weights, int32_t radius, double gain, double* out,
                           void* stream) {
@@ -920,51 +1106,11 @@ rf_status rf_blurriness(const double* gray, int32_t width, int32_t height, doubl
   keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const long long n = static_cast<long long>(width) * height;
-  double *b = nullptr, *buf = nullptr, *sums = nullptr;
-  bool ok = cudaMallocAsync(&b, sizeof(double) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&buf, sizeof(double) * 4 * n, s) == cudaSuccess &&
-            cudaMallocAsync(&sums, sizeof(double) * 4, s) == cudaSuccess;
-  rf_status st = ok ? RF_OK : RF_CUDA;
-  if (ok) {
-    // per axis: d_f and v = max(0, d_f - d_b), then the four pairwise sums at once
-    const double* arr[4];
-    long long cnt[4];
-    double* outs[4];
-    int axes = 0;
-    for (int axis = 0; axis < 2; ++axis) {
-      const int len = axis == 0 ? height : width;
-      if (len < 2) continue;
-      const int lines = axis == 0 ? width : height;
-      double* d_f = buf + 2 * axes * n;
-      double* vv = d_f + n;
-      if (len <= kBlurMaxLen) {
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(k_blur_lines_smem, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sizeof(double) * 2 * kBlurMaxLen * kBlurWarps));
-          attr = true;
-        }
-        k_blur_lines_smem<<<(lines + kBlurWarps - 1) / kBlurWarps, 32 * kBlurWarps,
-                            sizeof(double) * 2 * len * kBlurWarps, s>>>(gray, width, height, axis,
-                                                                       9, b, d_f, vv);
-      } else {
-        k_blur_lines<<<(lines + 63) / 64, 64, 0, s>>>(gray, width, height, axis, 9, b, d_f, vv);
-      }
-      const long long m = axis == 0 ? static_cast<long long>(height - 1) * width
-                                    : static_cast<long long>(height) * (width - 1);
-      arr[2 * axes] = d_f;
-      arr[2 * axes + 1] = vv;
-      cnt[2 * axes] = cnt[2 * axes + 1] = m;
-      outs[2 * axes] = sums + 2 * axes;
-      outs[2 * axes + 1] = sums + 2 * axes + 1;
-      ++axes;
-    }
-    if (axes > 0 && pairwise_sums(2 * axes, arr, cnt, outs, s) != RF_OK) st = RF_CUDA;
-    k_blur_finish<<<1, 1, 0, s>>>(sums, axes, blur_weight);
-  }
-  void* bufs[] = {b, buf, sums};
-  for (void* p : bufs)
-    if (p) cudaFreeAsync(p, s);
+  double* scratch = nullptr;
+  if (cudaMallocAsync(&scratch, sizeof(double) * (5 * n + 4), s) != cudaSuccess) return RF_CUDA;
+  const rf_status st = blurriness_core(gray, width, height, scratch, scratch + n,
+                                       scratch + 5 * n, blur_weight, s);
+  cudaFreeAsync(scratch, s);
   if (st != RF_OK) return st;
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }

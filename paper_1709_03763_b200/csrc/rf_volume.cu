@@ -442,6 +442,35 @@ void memo_release(rf_volume* v) {
   v->memo_slot_cap = 0;
 }
 
+// Per-keyframe key capacity of a memo slot for npix-pixel keyframes (a
+// sharded volume's entries hold the WHOLE footprint -- the contract is
+// checked on every key -- recorded by its sampling pass, duplicates across
+// pixel tiles included: room for one key per pixel).
+int memo_cap_for(const rf_volume* v, long long npix) {
+  return static_cast<int>(
+      v->cfg.shard_count > 1 ? std::max(4096LL, npix)
+                             : std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
+}
+
+// The memo arena, slots sized for `cap` keys each (allocated once).
+bool memo_arena_alloc(rf_volume* v, int cap) {
+  const size_t head = (sizeof(FpEntry) + 15) & ~size_t(15);
+  const size_t slot = (head + sizeof(long long) * static_cast<size_t>(cap) + 255) & ~size_t(255);
+  const size_t n = v->memo_budget / slot;
+  if (n == 0) return false;
+  if (cudaMalloc(&v->memo_arena, n * slot) != cudaSuccess) {
+    cudaGetLastError();
+    v->memo_arena = nullptr;
+    v->memo_budget = 0;  // no memo on this device
+    return false;
+  }
+  v->memo_slot_bytes = slot;
+  v->memo_slot_cap = cap;
+  v->memo_free.clear();
+  for (size_t i = n; i-- > 0;) v->memo_free.push_back(static_cast<int>(i));
+  return true;
+}
+
 // Returns the memo entry for (kf, pose) and whether it pre-existed.
 FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bool& existed) {
   existed = false;
@@ -456,26 +485,8 @@ FpEntry* memo_lookup(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose, bo
     existed = true;
     return it->second.dev;
   }
-  const long long npix = static_cast<long long>(kf->width) * kf->height;
-  const int cap = static_cast<int>(
-      v->cfg.shard_count > 1 ? std::max(4096LL, npix)
-                             : std::min<long long>(v->T.capacity, std::max(4096LL, npix / 3)));
-  const size_t head = (sizeof(FpEntry) + 15) & ~size_t(15);
-  if (!v->memo_arena) {  // first use: slots sized for this keyframe
-    const size_t slot = (head + sizeof(long long) * static_cast<size_t>(cap) + 255) & ~size_t(255);
-    const size_t n = v->memo_budget / slot;
-    if (n == 0) return nullptr;
-    if (cudaMalloc(&v->memo_arena, n * slot) != cudaSuccess) {
-      cudaGetLastError();
-      v->memo_arena = nullptr;
-      v->memo_budget = 0;  // no memo on this device
-      return nullptr;
-    }
-    v->memo_slot_bytes = slot;
-    v->memo_slot_cap = cap;
-    v->memo_free.clear();
-    for (size_t i = n; i-- > 0;) v->memo_free.push_back(static_cast<int>(i));
-  }
+  const int cap = memo_cap_for(v, static_cast<long long>(kf->width) * kf->height);
+  if (!v->memo_arena && !memo_arena_alloc(v, cap)) return nullptr;  // first use
   if (cap > v->memo_slot_cap) return nullptr;
   if (v->memo_free.empty()) {
     if (v->memo_lru.empty()) return nullptr;
@@ -532,6 +543,30 @@ void launch_fuse(rf_volume* v, const FuseParams& p) {
 // an earlier window).  Returns the slot per view (-1: device view).
 constexpr int kStageSlots = 16;
 
+// Room for `need` doubles in a staging slot (+ its events).  Growing
+// synchronises the device (cudaFree): a connected shard reserves its slots
+// up front (rf_reserve) so no call of the lockstep phase grows one while a
+// peer waits in k_shard_sync.
+template <typename Slot>
+rf_status stage_slot_grow(rf_volume* v, Slot& sl, size_t need) {
+  if (!v->copy_stream)
+    RF_CUDA_TRY(v, cudaStreamCreateWithFlags(&v->copy_stream, cudaStreamNonBlocking));
+  if (sl.cap < need) {
+    RF_CUDA_TRY(v, cudaStreamSynchronize(v->copy_stream));
+    RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
+    if (sl.buf) cudaFree(sl.buf);
+    sl.buf = nullptr;
+    RF_CUDA_TRY(v, cudaMalloc(&sl.buf, sizeof(double) * need));
+    sl.cap = need;
+  }
+  if (!sl.ready) RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
+  if (!sl.consumed)
+    RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
+  if (!sl.color_ready)
+    RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.color_ready, cudaEventDisableTiming));
+  return RF_OK;
+}
+
 rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_kf_view>& out,
                       std::vector<int>& slot_of) {
   out.assign(in, in + n);
@@ -561,19 +596,10 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
       v->stage_next = (v->stage_next + 1) % static_cast<int>(v->stage.size());
       auto& sl = v->stage[s];
       const size_t need = npix * (k.color ? 5 : 2);
-      if (sl.cap < need) {
-        RF_CUDA_TRY(v, cudaStreamSynchronize(v->copy_stream));
-        RF_CUDA_TRY(v, cudaStreamSynchronize(v->stream));
-        if (sl.buf) cudaFree(sl.buf);
-        sl.buf = nullptr;
-        RF_CUDA_TRY(v, cudaMalloc(&sl.buf, sizeof(double) * need));
-        sl.cap = need;
+      {
+        const rf_status gst = stage_slot_grow(v, sl, need);
+        if (gst != RF_OK) return gst;
       }
-      if (!sl.ready) RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.ready, cudaEventDisableTiming));
-      if (!sl.consumed)
-        RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.consumed, cudaEventDisableTiming));
-      if (!sl.color_ready)
-        RF_CUDA_TRY(v, cudaEventCreateWithFlags(&sl.color_ready, cudaEventDisableTiming));
       if (sl.used) cudaStreamWaitEvent(v->copy_stream, sl.consumed, 0);
       // depth + weight first: the footprint and the removal check need only
       // those, so they start while the colour plane is still in flight
@@ -1210,6 +1236,24 @@ rf_status rf_shard_sync_ipc_open(rf_volume* v, const void* handles) {
     v->sync_ipc[s] = true;
   }
   return rf_shard_sync_connect(v, ptrs.data());
+}
+
+rf_status rf_reserve(rf_volume* v, int32_t width, int32_t height, int32_t max_ops) {
+  if (!v || width <= 0 || height <= 0 || max_ops <= 0 || max_ops > kMaxWindowOps * 8 ||
+      static_cast<long long>(width) * height >= (1LL << 31))
+    return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  rf_status st = ensure_ops(v, max_ops);
+  if (st != RF_OK) return st;
+  const long long npix = static_cast<long long>(width) * height;
+  if (v->stage.size() < static_cast<size_t>(kStageSlots)) v->stage.resize(kStageSlots);
+  for (auto& sl : v->stage) {
+    st = stage_slot_grow(v, sl, static_cast<size_t>(npix) * 5);
+    if (st != RF_OK) return st;
+  }
+  if (v->memo_budget > 0 && !v->memo_arena) memo_arena_alloc(v, memo_cap_for(v, npix));
+  RF_CUDA_TRY(v, cudaDeviceSynchronize());
+  return RF_OK;
 }
 
 rf_status rf_allocate(rf_volume* v, const rf_kf_view* kf, const rf_pose* pose,

@@ -269,8 +269,19 @@ def depth_weight_map(depth, intr, delta_disc=DELTA_DISC):
 # colour prep (keyframe_fusion.py:303-346)
 
 
+_GAUSS = {}
+
+
 def _gauss_weights(sigma, truncate=4.0):
-    """scipy.ndimage._gaussian_kernel1d(sigma, 0, radius) -- host numpy, as scipy."""
+    """scipy.ndimage._gaussian_kernel1d(sigma, 0, radius) -- host numpy, as scipy
+    (cached per (sigma, truncate))."""
+    key = (float(sigma), float(truncate))
+    if key not in _GAUSS:
+        _GAUSS[key] = _gauss_weights_uncached(sigma, truncate)
+    return _GAUSS[key]
+
+
+def _gauss_weights_uncached(sigma, truncate=4.0):
     radius = int(truncate * float(sigma) + 0.5)
     sigma2 = sigma * sigma
     x = np.arange(-radius, radius + 1)
@@ -332,31 +343,38 @@ def weighted_median(values, weights):
 
 def fuse_depth(kf, frame, delta_disc=DELTA_DISC):
     """Warp one frame into the keyframe and apply the running weighted
-    average per target pixel; member buffers are retained on the device."""
+    average per target pixel; member buffers are retained on the device.
+    One native call per frame (rf_fuse_frame): weight map, depth copy, warp +
+    ordered scatter + Eq. 1 merge, colour prep."""
     if kf.finalized:
         raise ValueError("keyframe color already finalized; cannot add frames")
     torch = _torch()
     intr = kf.intrinsics
     h, w = intr.height, intr.width
     depth = _plane(frame.depth, (h, w))
-    w_map = depth_weight_map(depth, intr, delta_disc)
+    w_map = torch.empty_like(depth)
+    depth_copy = torch.empty_like(depth)
     rel = pose_struct(compose(inverse(kf.pose), frame.pose))
-    _check(L.lib().rf_fuse_depth(kf.depth.data_ptr(), kf.weight.data_ptr(), depth.data_ptr(),
-                                 w_map.data_ptr(), w, h, float(intr.fx), float(intr.fy),
-                                 float(intr.cx), float(intr.cy), ctypes.byref(rel),
-                                 detect_blas_order(), _stream()), "rf_fuse_depth")
-    blur = torch.ones((), dtype=torch.float64, device=depth.device)
     member_color = None
+    color = None
     if frame.color is not None:
         color = _plane(frame.color, (h, w, 3))
         member_color = torch.empty_like(color)
-        wts, radius = _gauss_weights(UNSHARP_SIGMA)
-        _check(L.lib().rf_color_prep(color.data_ptr(), w, h, wts.ctypes.data_as(L.c_double_p),
-                                     radius, UNSHARP_GAIN, member_color.data_ptr(),
-                                     blur.data_ptr(), _stream()), "rf_color_prep")
+        blur = torch.empty((), dtype=torch.float64, device=depth.device)
+    else:
+        blur = torch.ones((), dtype=torch.float64, device=depth.device)
+    wts, radius = _gauss_weights(UNSHARP_SIGMA)
+    _check(L.lib().rf_fuse_frame(
+        kf.depth.data_ptr(), kf.weight.data_ptr(), depth.data_ptr(),
+        color.data_ptr() if color is not None else None, w, h, float(intr.fx),
+        float(intr.fy), float(intr.cx), float(intr.cy), ctypes.byref(rel), detect_blas_order(),
+        float(delta_disc), wts.ctypes.data_as(L.c_double_p), radius, UNSHARP_GAIN,
+        w_map.data_ptr(), depth_copy.data_ptr(),
+        member_color.data_ptr() if member_color is not None else None,
+        blur.data_ptr() if color is not None else None, _stream()), "rf_fuse_frame")
     kf.members.append(frame.index)
     kf.observations.append(_MemberObservation(
-        index=frame.index, color=member_color, depth=depth.clone(), pose=frame.pose.copy(),
+        index=frame.index, color=member_color, depth=depth_copy, pose=frame.pose.copy(),
         blur_weight=blur, weight_map=w_map))
     return kf
 

@@ -245,3 +245,35 @@ def render_keyframe(renderer, pose, seed, kappa=5):
     weight = torch.where(valid, kappa / torch.clamp(depth * depth, min=1e-12),
                          torch.zeros_like(depth))
     return DeviceKeyframe(renderer.intr, pose, depth, weight, color)
+
+
+def fused_keyframe(renderer, gt_frames, est_frames, seeds, first_index=1):
+    """A keyframe fused from a burst of rendered frames, the way
+    pipeline.run_pipeline builds one (/root/reference/pkg/src/refusion/
+    pipeline.py:204-271): frame j is rendered at its ground-truth pose
+    ``gt_frames[j]`` (noise seed ``seeds[j]``) and fused at its estimated
+    pose ``est_frames[j]`` (keyframe_fusion.new_keyframe / fuse_depth), then
+    the colour is finalised (fuse_color).  Returns a DeviceKeyframe at
+    ``est_frames[0]`` holding the fused depth / weight / colour planes."""
+    from . import keyframe_fusion as KF
+
+    kf = None
+    for j, (g, e, s) in enumerate(zip(gt_frames, est_frames, seeds)):
+        depth, color = renderer.render(g, seed=s)
+        obs = KF.FrameObservation(index=first_index + j, color=color, depth=depth, pose=e)
+        if kf is None:
+            kf = KF.new_keyframe(obs, renderer.intr)
+        KF.fuse_depth(kf, obs)
+    KF.fuse_color(kf)
+    return DeviceKeyframe(renderer.intr, kf.pose, kf.depth, kf.weight, kf.color)
+
+
+def burst_poses(gt_frames, kf_first, drifted_kf, kappa):
+    """Estimated poses of the frames of keyframe k: the keyframe's drift
+    (drifted_kf[k] vs gt_frames[k * kappa]) applied rigidly to its burst,
+    so relative poses inside a burst are exact."""
+    from .geometry import inverse
+
+    k0 = kf_first * kappa
+    corr = compose(drifted_kf, inverse(gt_frames[k0]))
+    return [drifted_kf.copy()] + [compose(corr, gt_frames[k0 + j]) for j in range(1, kappa)]

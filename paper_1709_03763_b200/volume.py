@@ -299,6 +299,7 @@ class TwoTierStore:
         self._cfg = None
         self._pending = None  # blocks loaded before the store was bound
         self._router = None   # routed footprints (connect_shards*)
+        self._own_stream = None  # a private stream (shards emulated in one process)
 
     # -- binding ------------------------------------------------------------
     def _bind(self, cfg):
@@ -341,6 +342,18 @@ class TwoTierStore:
     def _call_status(self, name, *args):
         torch = _torch()
         lib = L.lib()
+        if self._own_stream is not None:
+            # a shard with its own stream: ordered after the caller's stream
+            # and before the caller's later work, but never queued behind a
+            # sibling shard's kernels (which may wait in k_shard_sync for it)
+            with torch.cuda.device(self.device):
+                cur = torch.cuda.current_stream()
+                own = self._own_stream
+                own.wait_stream(cur)
+                lib.rf_set_cuda_stream(self._ptr, own.cuda_stream)
+                st = getattr(lib, name)(self._ptr, *args)
+                cur.wait_stream(own)
+                return st
         if torch.cuda.current_device() == self.device:  # the common case: no context switch
             lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
             return getattr(lib, name)(self._ptr, *args)
@@ -795,8 +808,16 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
     if G < 2 or any(s.shard_count != G for s in stores) or \
             sorted(s.shard_rank for s in stores) != list(range(G)):
         raise ValueError("connect_shards needs one store per shard rank 0..G-1")
+    import torch
+
     for s in stores:
         s._bind(cfg)
+        # each shard runs on its own stream: shards sharing one device must
+        # not queue behind each other's kernels (k_shard_sync waits for every
+        # shard's check), and nothing of the lockstep phase may allocate
+        with torch.cuda.device(s.device):
+            s._own_stream = torch.cuda.Stream()
+        s._call("rf_reserve", image[0], image[1], _SYNC_OPS)
     # cross-shard removal verdicts (k_shard_sync): every de-integration fails
     # on all shards at the same op with the same key, as one volume would
     slots = {s.shard_rank: _sync_setup(s) for s in stores}
@@ -838,6 +859,7 @@ def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640
 
     G = store.shard_count
     store._bind(cfg)
+    store._call("rf_reserve", image[0], image[1], _SYNC_OPS)
     # cross-shard removal verdicts: slots exchanged once as CUDA IPC handles
     _sync_setup(store)
     h = (ctypes.c_char * 64)()

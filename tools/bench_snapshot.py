@@ -31,13 +31,13 @@ def main():
     from paper_1709_03763_b200 import volume as V
 
     torch.cuda.set_device(0)
-    gt_kf, drifted = B.kf_poses(args.keyframes)
-    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=0)
+    gt, gt_kf, drifted = B.kf_poses(args.keyframes)
+    kfs = B.build_keyframes(args.keyframes, gt, drifted)
     cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
                          hash_buckets=1 << 21)
     store = V.TwoTierStore(block_capacity=1_500_000)
     for k in range(args.keyframes):
-        kf = SY.render_keyframe(rend, gt_kf[k], seed=1000 + k, kappa=B.KAPPA)
+        kf = kfs[k]
         V.stream(store, drifted[k].translation, cfg)
         V.integrate(store, kf, drifted[k], cfg)
     torch.cuda.synchronize()

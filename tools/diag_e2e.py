@@ -16,9 +16,8 @@ from paper_1709_03763_b200 import volume as V  # noqa: E402
 
 torch.cuda.set_device(0)
 n = 40
-gt, dr = bench.kf_poses(n)
-rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS)
-kfs = [SY.render_keyframe(rend, gt[k], seed=1000 + k) for k in range(n)]
+gt_f, gt, dr = bench.kf_poses(n)
+kfs = bench.build_keyframes(n, gt_f, dr)
 host = [k.to_host(pinned=True) for k in kfs]
 torch.cuda.synchronize()
 # 1. H2D bandwidth, 10 keyframes' planes

@@ -26,13 +26,8 @@ def main():
     torch.cuda.set_device(0)
     n_kf = int(os.environ.get("KF", "200"))
     steps = 8
-    gt, dr = B.kf_poses(n_kf)
-    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=0)
-    kfs = []
-    for k in range(n_kf):
-        kf = SY.render_keyframe(rend, gt[k], seed=1000 + k, kappa=B.KAPPA)
-        kf.pose = dr[k]
-        kfs.append(kf)
+    gt_f, gt, dr = B.kf_poses(n_kf)
+    kfs = B.build_keyframes(n_kf, gt_f, dr)
     cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
                          hash_buckets=1 << 21)
     store = V.TwoTierStore(block_capacity=2_000_000)

@@ -15,9 +15,8 @@ from paper_1709_03763_b200 import volume as V  # noqa: E402
 
 torch.cuda.set_device(0)
 n = 20
-gt, dr = bench.kf_poses(n)
-rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS)
-kfs = [SY.render_keyframe(rend, gt[k], seed=1000 + k) for k in range(n)]
+gt_f, gt, dr = bench.kf_poses(n)
+kfs = bench.build_keyframes(n, gt_f, dr)
 cfg = V.VolumeConfig(voxel_size=bench.VOXEL, mu=bench.MU, stream_radius=bench.RADIUS,
                      hash_buckets=1 << 21)
 store = V.TwoTierStore(block_capacity=1_000_000)

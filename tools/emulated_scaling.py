@@ -55,13 +55,8 @@ def main():
 
     torch.cuda.set_device(0)
     lib = L.lib()
-    gt_kf, drifted = B.kf_poses(args.keyframes)
-    rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS, device=0)
-    kfs = []
-    for k in range(args.keyframes):
-        kf = SY.render_keyframe(rend, gt_kf[k], seed=1000 + k, kappa=B.KAPPA)
-        kf.pose = drifted[k]
-        kfs.append(kf)
+    gt, gt_kf, drifted = B.kf_poses(args.keyframes)
+    kfs = B.build_keyframes(args.keyframes, gt, drifted)
     torch.cuda.synchronize()
     voxel = args.voxel or B.VOXEL
     cfg = V.VolumeConfig(voxel_size=voxel, mu=B.MU, stream_radius=B.RADIUS,

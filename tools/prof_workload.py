@@ -29,9 +29,8 @@ ap.add_argument("--json", default=None)
 a = ap.parse_args()
 
 torch.cuda.set_device(0)
-gt_kf, drifted = bench.kf_poses(400)
-rend = SY.Renderer(SY.corridor_scene(), SY.DEFAULT_INTRINSICS)
-kfs = [SY.render_keyframe(rend, gt_kf[k], seed=1000 + k) for k in range(a.build)]
+gt, gt_kf, drifted = bench.kf_poses(400)
+kfs = bench.build_keyframes(a.build, gt, drifted)  # the bench's fused keyframes
 cfg = V.VolumeConfig(voxel_size=a.voxel, mu=bench.MU, stream_radius=bench.RADIUS,
                      hash_buckets=1 << 21)
 store = V.TwoTierStore(block_capacity=600_000)
