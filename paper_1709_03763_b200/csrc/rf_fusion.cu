@@ -475,15 +475,19 @@ __global__ void __launch_bounds__(32 * kBlurWarps)
   double* s_out = s_in + len;
   for (int k = lane; k < len; k += 32) s_in[k] = src[static_cast<size_t>(k) * stride];
   __syncwarp();
+  const int s1 = size / 2;
+  auto at = [&](int k) { return s_in[min(max(k, 0), len - 1)]; };
+  // the running sum's increments (x[l+size-1-s1] - x[l-1-s1]), rounded as
+  // scipy rounds them, computed by all lanes; lane 0 then only chains adds
+  for (int l = 1 + lane; l < len; l += 32) s_out[l] = at(l + size - 1 - s1) - at(l - 1 - s1);
+  __syncwarp();
   if (lane == 0) {  // the running sums (sequential); the lanes divide below
-    const int s1 = size / 2;
-    auto at = [&](int k) { return s_in[min(max(k, 0), len - 1)]; };
     double tmp = 0.0;
     for (int l = 0; l < size; ++l) tmp = tmp + at(l - s1);
     s_out[0] = tmp;
-#pragma unroll 8
+#pragma unroll 16
     for (int l = 1; l < len; ++l) {
-      tmp = tmp + (at(l + size - 1 - s1) - at(l - 1 - s1));
+      tmp = tmp + s_out[l];
       s_out[l] = tmp;
     }
   }

@@ -529,9 +529,53 @@ struct RouteConsume {
 };
 
 // Launch the batched fuse kernel of mode kMode.
+#if RF_KF_TMA
+// Tensor map of one f64 keyframe plane [height][width] with the kTileW x
+// kTileH box of the fuse kernels' keyframe tiles (cuTensorMapEncodeTiled
+// through the runtime's driver entry point; no -lcuda).
+bool plane_tensor_map(CUtensorMap* m, const double* base, int width, int height) {
+  using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static Encode fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<Encode>(f);
+  }
+  std::memset(m, 0, sizeof(*m));
+  if (!base || (reinterpret_cast<uintptr_t>(base) & 15) || (width * 8) % 16 || width < kTileW ||
+      height < kTileH)
+    return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(width), static_cast<cuuint64_t>(height)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(width) * 8};
+  const cuuint32_t box[2] = {kTileW, kTileH};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr size_t kFuseDynSmem = static_cast<size_t>(kFuseThreads / 32) * kTileWarpBytes;
+#endif
+
+// Launch the batched fuse kernel of mode kMode.
 template <int kMode>
 void launch_fuse(rf_volume* v, const FuseParams& p) {
+#if RF_KF_TMA
+  CUtensorMap md, mw;
+  FuseParams q = p;
+  q.kf_tma = plane_tensor_map(&md, p.kf.depth, p.kf.width, p.kf.height) &&
+             plane_tensor_map(&mw, p.kf.weight, p.kf.width, p.kf.height);
+  launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, kFuseDynSmem, v->stream, v->T, q,
+         md, mw);
+#else
   launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
+#endif
 }
 
 // Host keyframe planes (planes_on_host): copy each distinct keyframe of a
@@ -899,10 +943,19 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
     }
   }
   int occ[4] = {1, 1, 1, 1};
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, 0);
+#if RF_KF_TMA
+  const size_t dsm = kFuseDynSmem;
+  cudaFuncSetAttribute(k_fuse<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+  cudaFuncSetAttribute(k_fuse<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+  cudaFuncSetAttribute(k_fuse<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+  cudaFuncSetAttribute(k_fuse<kRemoveReadd>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
+#else
+  const size_t dsm = 0;
+#endif
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, dsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, dsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, dsm);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, dsm);
   for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;

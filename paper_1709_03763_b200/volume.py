@@ -85,15 +85,45 @@ class VoxelBlock:
         return VoxelBlock(self.coord, self.d.copy(), self.w.copy(), self.c.copy())
 
 
-@dataclass(frozen=True)
 class IntegrationRecord:
-    """volume.py:126-134"""
+    """volume.py:126-134 -- (kf, pose, new_blocks, blocks_touched,
+    voxels_updated), immutable.  ``new_blocks`` (a frozenset of coordinate
+    tuples) is built from the device's packed keys on first access: a fresh
+    keyframe can create tens of thousands of blocks, and most callers never
+    look at them."""
 
-    kf: object
-    pose: object
-    new_blocks: frozenset = field(default_factory=frozenset)
-    blocks_touched: int = 0
-    voxels_updated: int = 0
+    __slots__ = ("kf", "pose", "blocks_touched", "voxels_updated", "_keys", "_new")
+
+    def __init__(self, kf, pose, new_blocks=frozenset(), blocks_touched=0, voxels_updated=0,
+                 new_keys=None):
+        for k, v in (("kf", kf), ("pose", pose), ("blocks_touched", blocks_touched),
+                     ("voxels_updated", voxels_updated), ("_keys", new_keys),
+                     ("_new", None if new_keys is not None else frozenset(new_blocks))):
+            object.__setattr__(self, k, v)
+
+    @property
+    def new_blocks(self):
+        if self._new is None:
+            object.__setattr__(self, "_new", frozenset(keys_to_coords(self._keys)))
+        return self._new
+
+    def __setattr__(self, name, value):
+        raise AttributeError(f"IntegrationRecord is immutable ({name})")
+
+    def __eq__(self, other):
+        if not isinstance(other, IntegrationRecord):
+            return NotImplemented
+        return (self.kf is other.kf or self.kf == other.kf) and self.pose == other.pose and \
+            self.new_blocks == other.new_blocks and \
+            self.blocks_touched == other.blocks_touched and \
+            self.voxels_updated == other.voxels_updated
+
+    __hash__ = None
+
+    def __repr__(self):
+        n = len(self._keys) if self._new is None else len(self._new)
+        return (f"IntegrationRecord(kf={self.kf!r}, pose={self.pose!r}, new_blocks=<{n} blocks>, "
+                f"blocks_touched={self.blocks_touched}, voxels_updated={self.voxels_updated})")
 
 
 def block_hash(coord, buckets):
@@ -585,7 +615,7 @@ def integrate(store, kf, pose, cfg):
     return IntegrationRecord(
         kf=kf,
         pose=pose.copy(),
-        new_blocks=frozenset(keys_to_coords(new[: int(res.n_new)])),
+        new_keys=new[: int(res.n_new)].copy(),
         blocks_touched=int(res.blocks_touched),
         voxels_updated=int(res.voxels_updated),
     )
