@@ -263,9 +263,9 @@ def run_b200(args):
     def prepare():
         """Host side of a pose-graph update (not part of the correction's
         wall time): merge the event, pick the top-m entries."""
-        t = time.perf_counter()
-        ev = scen.event(step_idx[0])
+        ev = scen.event(step_idx[0])  # the pose-graph backend's output (input here)
         step_idx[0] += 1
+        t = time.perf_counter()
         R.apply_pose_update(scen.ledger, ev)
         picks = R.select_topk(scen.ledger, args.m)
         nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation

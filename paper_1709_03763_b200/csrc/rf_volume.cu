@@ -560,7 +560,7 @@ bool plane_tensor_map(CUtensorMap* m, const double* base, int width, int height)
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-constexpr size_t kFuseDynSmem = static_cast<size_t>(kFuseThreads / 32) * kTileWarpBytes;
+constexpr size_t kFuseDynSmem = static_cast<size_t>(kFuseThreads / 32) * kTileWarpBytes + 128;
 #endif
 
 // Launch the batched fuse kernel of mode kMode.

@@ -161,3 +161,96 @@ def ray_grid(k):
     dir_x = np.broadcast_to((u - k.cx) / k.fx, (k.height, k.width))
     dir_y = np.broadcast_to(((v - k.cy) / k.fy)[:, None], (k.height, k.width))
     return np.ascontiguousarray(dir_x), np.ascontiguousarray(dir_y)
+
+
+# ---------------------------------------------------------------------------
+# batched host pose algebra for the correction scheduler: the same numpy
+# operations as compose / euler_zyx / pose_distance above, over stacks.  A
+# stacked np.matmul runs the scalar call's BLAS kernel per matrix, and the
+# ufuncs run elementwise, so the results are the same bits; batch_exact()
+# checks that once on this host (BLAS builds and SIMD ufunc loops differ
+# between machines) and the callers fall back to the per-pose path if not.
+
+_BATCH_OK = None
+
+
+def compose_many(Ts, Us):
+    """[compose(T, U) for T, U in zip(Ts, Us)] -- one batched matmul; poses
+    whose validation lands within 1e-12 of the tolerance (or fails) are
+    rebuilt with the checked constructor."""
+    n = len(Us)
+    if n == 0:
+        return []
+    RT = np.array([T.rotation for T in Ts])
+    R = np.matmul(RT, np.array([U.rotation for U in Us]))
+    t = np.matmul(RT, np.array([U.translation for U in Us])[..., None])[..., 0] + \
+        np.array([T.translation for T in Ts])
+    err = np.abs(np.matmul(R.transpose(0, 2, 1), R) - _EYE3).max(axis=(1, 2))
+    a, b, c = R[:, 0, 0], R[:, 0, 1], R[:, 0, 2]
+    d, e, f = R[:, 1, 0], R[:, 1, 1], R[:, 1, 2]
+    g, h, i = R[:, 2, 0], R[:, 2, 1], R[:, 2, 2]
+    dev = np.abs(a * (e * i - f * h) - b * (d * i - f * g) + c * (d * h - e * g) - 1.0)
+    safe = (err < ORTHONORMAL_TOL - 1e-12) & (np.abs(dev - ORTHONORMAL_TOL) >= 1e-9) & \
+        (dev <= ORTHONORMAL_TOL)
+    out = []
+    for k in range(n):
+        if safe[k]:
+            p = object.__new__(Pose)
+            p.rotation = R[k].copy()
+            p.translation = t[k].copy()
+        else:
+            p = Pose(R[k], t[k])  # the exact checks (and their errors)
+        out.append(p)
+    return out
+
+
+def euler_zyx_many(R):
+    """euler_zyx over a stack [n][3][3] -> [n][3]."""
+    sp = np.minimum(1.0, np.maximum(-1.0, -R[:, 2, 0]))
+    pitch = np.arcsin(sp)
+    reg = np.abs(sp) < 1.0 - 1e-12
+    yaw = np.where(reg, np.arctan2(R[:, 1, 0], R[:, 0, 0]), np.arctan2(-R[:, 0, 1], R[:, 1, 1]))
+    roll = np.where(reg, np.arctan2(R[:, 2, 1], R[:, 2, 2]), 0.0)
+    return np.stack([yaw, pitch, roll], axis=1)
+
+
+def pose_distance_many(As, Bs, s=DEFAULT_DISTANCE_SCALE):
+    """[pose_distance(A, B, s)] over two lists of poses."""
+    n = len(As)
+    if n == 0:
+        return np.empty(0)
+    ea = euler_zyx_many(np.array([p.rotation for p in As]))
+    eb = euler_zyx_many(np.array([p.rotation for p in Bs]))
+    tA = np.array([p.translation for p in As])
+    tB = np.array([p.translation for p in Bs])
+    D = np.concatenate([wrap_angle(ea - eb), tA - tB], axis=1) * np.asarray(s, dtype=np.float64)
+    return np.sqrt(np.array([np.dot(r, r) for r in D]))  # np.linalg.norm: sqrt(dot(x, x))
+
+
+def batch_exact():
+    """Do the batched forms give the per-pose bits on this host?  (cached)"""
+    global _BATCH_OK
+    if _BATCH_OK is None:
+        rng = np.random.default_rng(20261017)
+        ok = True
+        for _ in range(4):
+            def rp(scale):
+                q = rng.normal(size=4)
+                q /= np.linalg.norm(q)
+                w, x, y, z = q
+                R = np.array([[1 - 2 * (y * y + z * z), 2 * (x * y - z * w), 2 * (x * z + y * w)],
+                              [2 * (x * y + z * w), 1 - 2 * (x * x + z * z), 2 * (y * z - x * w)],
+                              [2 * (x * z - y * w), 2 * (y * z + x * w), 1 - 2 * (x * x + y * y)]])
+                return Pose(R, rng.normal(size=3) * scale)
+            T = rp(3.0)
+            rels = [rp(1.0) for _ in range(33)]
+            many = compose_many([T] * len(rels), rels)
+            one = [compose(T, U) for U in rels]
+            ok &= all(np.array_equal(a.rotation, b.rotation) and
+                      np.array_equal(a.translation, b.translation) for a, b in zip(many, one))
+            others = [rp(2.0) for _ in range(33)]
+            dm = pose_distance_many(one, others)
+            ds = np.array([pose_distance(a, b) for a, b in zip(one, others)])
+            ok &= bool(np.array_equal(dm, ds))
+        _BATCH_OK = bool(ok)
+    return _BATCH_OK
