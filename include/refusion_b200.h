@@ -216,6 +216,22 @@ rf_status rf_marching_cubes_welded(rf_volume *vol, double tol, double *vertices,
  * NULL.  Needs no volume. */
 rf_status rf_nn_min_d2(const double *q, int64_t n, const double *pts, int64_t m, double *out,
                        void *stream);
+
+/* ---- evaluation: exact nearest-neighbour grid index ------
+ * GridIndex of /root/reference/pkg/src/refusion/evaluation.py:108-229 on the
+ * device: points bucketed into cells of cell_size (floor(p / cell_size),
+ * packed like _pack_cells), queries scan rings of cells outward and fall
+ * back to the exact linear scan exactly where the reference does; every
+ * distance is the IEEE sqrt of the exact minimum of (dx*dx + dy*dy) + dz*dz
+ * over the indexed points, bit-identical to the reference.  points, queries
+ * and out are DEVICE pointers ([n][3], [m][3], [m] f64); the index owns a
+ * sorted copy of the points. */
+typedef struct rf_grid_index rf_grid_index;
+rf_status rf_grid_index_create(const double *points, int64_t n, double cell_size,
+                               rf_grid_index **index, void *stream);
+rf_status rf_grid_index_query(rf_grid_index *index, const double *queries, int64_t m,
+                              double *out, void *stream);
+rf_status rf_grid_index_destroy(rf_grid_index *index);
 /* save_volume's SDFV1 records (volume.py:397-415), streamed: records_host
  * receives blocks [first, first + count) in sorted coordinate order, each
  * 3 x int32 coordinate + 512 x 5 f64 (D, W, C0, C1, C2 per voxel) = 20,492 B,

@@ -185,6 +185,10 @@ SIGNATURES = {
     "rf_export_blocks": (_S, [_vp, c_int64_p, c_double_p, ctypes.c_int64, c_int64_p]),
     "rf_import_blocks": (_S, [_vp, c_int64_p, c_double_p, ctypes.c_int64]),
     "rf_snapshot_records": (_S, [_vp, ctypes.c_int64, ctypes.c_int64, _vp, c_int64_p]),
+    "rf_grid_index_create": (_S, [_vp, ctypes.c_int64, ctypes.c_double, ctypes.POINTER(_vp),
+                                  _vp]),
+    "rf_grid_index_query": (_S, [_vp, _vp, ctypes.c_int64, _vp, _vp]),
+    "rf_grid_index_destroy": (_S, [_vp]),
     "rf_nn_min_d2": (_S, [c_double_p, ctypes.c_int64, c_double_p, ctypes.c_int64, c_double_p,
                           _vp]),
     "rf_marching_cubes_welded": (_S, [_vp, ctypes.c_double, c_double_p, c_double_p, c_int64_p,

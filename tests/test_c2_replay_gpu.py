@@ -72,7 +72,8 @@ def test_c2_topk_replay_matches_oracle():
     from paper_1709_03763_b200 import volume as V
 
     torch.cuda.set_device(0)
-    gt, gt_kf, drifted = B.kf_poses(N_KF)
+    gt, gt_kf, drifted = B.kf_poses(B.N_FRAMES // B.KAPPA)  # the bench trajectory
+    gt_kf, drifted = gt_kf[:N_KF], drifted[:N_KF]
     kfs = B.build_keyframes(N_KF, gt, drifted)
     cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
                          hash_buckets=1 << 20)
