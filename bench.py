@@ -174,7 +174,9 @@ def kf_poses(n_kf):
 
 
 def frame_seed(j):
-    return 1000 + j
+    """numpy seed of frame j's depth noise -- make_sequence's (seed, 7, index)
+    form; the reference arm renders its frames with the same seeds."""
+    return (1, 7, j)
 
 
 def build_keyframes(n_kf, gt, drifted, device=0, rank=0, world=1):
@@ -463,8 +465,9 @@ def run_b200(args):
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (GPU sphere-traced analytic corridor, sigma0 z^2 depth noise; "
-                "keyframes fused on the device from 5 rendered frames each)",
+        "data": "synthetic (the reference's synth.py renderer ported bit-exact to the device: "
+                "sphere-traced analytic corridor, numpy sigma0 z^2 depth noise with the reference "
+                "arm's seeds; keyframes fused on the device from 5 rendered frames each)",
         "config": {"workload": WORKLOAD, "keyframes": n_kf, "m": args.m,
                    "voxel_size": VOXEL, "mu": MU, "stream_radius": RADIUS,
                    "hash_buckets": cfg.hash_buckets, "blocks_resident": n_blocks,

@@ -210,6 +210,23 @@ rf_status rf_marching_cubes(rf_volume *vol, double *vertices, double *colors, in
 rf_status rf_marching_cubes_welded(rf_volume *vol, double tol, double *vertices, double *colors,
                                    int64_t *triangles, int64_t vcap, int64_t tcap, int64_t *nv,
                                    int64_t *nt);
+/* Cross-shard marching cubes (meshing.py:112-147 borrows the +x/+y/+z
+ * neighbour blocks): on a hash-sharded volume a neighbour may be owned by
+ * another shard; once connected, each shard's marching cubes reads those
+ * neighbours' corners from the owner's pool (same device, or NVLink peers
+ * mapped by CUDA IPC), so the union of the shards' meshes is the unsharded
+ * mesh.  rf_mesh_connect: in-process shards (shards[rank] == vol).
+ * rf_mesh_ipc_handle: this shard's four table allocations (heads, keys,
+ * next, pool) as 4 cudaIpcMemHandle_t (256 bytes).  rf_mesh_ipc_open: every
+ * shard's 4 handles [count][4] (own entry ignored) and hash_buckets. */
+rf_status rf_mesh_connect(rf_volume *vol, rf_volume *const *shards, int32_t count);
+rf_status rf_mesh_ipc_handle(rf_volume *vol, void *handles);
+rf_status rf_mesh_ipc_open(rf_volume *vol, const void *handles, const int64_t *buckets);
+/* The per-block layout of rf_marching_cubes' output: the store's block keys
+ * in sorted order with each block's vertex / triangle counts (to merge the
+ * shards' meshes into the unsharded order).  Sizing protocol as above. */
+rf_status rf_mesh_blocks(rf_volume *vol, int64_t *keys, int64_t *vcounts, int64_t *tcounts,
+                         int64_t cap, int64_t *n_out);
 /* nn_min_d2 (_kernels_cy.pyx:111-129; refusion.kernels.nn_min_d2): out[i] =
  * min_j (dx*dx + dy*dy) + dz*dz over pts, q [n][3] / pts [m][3] / out [n]
  * HOST arrays (copied through the device); +inf when m == 0.  stream may be
@@ -435,24 +452,45 @@ typedef struct rf_synth_prim {
     double albedo[3];
 } rf_synth_prim;
 
-typedef struct rf_synth_params {
-    double z_max;        /* synth.py:29 */
+/* Faithful renderer: render_depth / render_color of
+ * synth.py:220-267 bit for bit (numpy's evaluation order; the two BLAS
+ * products in the host's calibrated order).  Depth noise is drawn on the
+ * host by numpy (synth.py:270-283, PCG64 stream); colour shades the noisy
+ * depth as make_sequence does. */
+typedef struct rf_synth_ref_params {
+    double z_max;        /* render_depth z_max (Z_MAX_DEFAULT 10.0) */
     double tol;          /* SPHERE_TRACE_TOL */
-    double sigma0;       /* depth noise sigma0 * z^2 (0 = none) */
-    double ambient, diffuse;
-    double light[3];     /* unit light direction */
-    uint64_t seed;
+    double ambient, diffuse;   /* AMBIENT, DIFFUSE */
+    double neg_light[3]; /* -light_dir (render_color's normal @ (-light_dir)) */
+    double normal_eps;   /* _NORMAL_EPS */
     int32_t steps;       /* SPHERE_TRACE_STEPS */
+    int32_t gemm_order;  /* rf_blas_order of (n,3) @ (3,3) on the host */
+    int32_t gemv_order;  /* rf_blas_order of (n,3) @ (3,) on the host */
     int32_t _pad;
-} rf_synth_params;
+} rf_synth_ref_params;
 
-/* Render z-depth [h][w] and colour [h][w][3] (colour may be NULL) of an
- * analytic scene; prims, depth and colour are device pointers. */
-rf_status rf_synth_render(const rf_synth_prim *prims_dev, int32_t n_prims,
-                          const rf_pose *pose, double fx, double fy, double cx,
-                          double cy, int32_t width, int32_t height,
-                          const rf_synth_params *params, double *depth_dev,
-                          double *color_dev, void *stream);
+typedef struct rf_synth_gauss {
+    double w[64];        /* w[0] centre, w[j] weight at offset j (symmetric) */
+    int32_t r;           /* radius (<= 63) */
+    int32_t _pad;
+} rf_synth_gauss;
+
+/* render_depth (synth.py:220-250): z-depth [h][w] on the device */
+rf_status rf_synth_depth(const rf_synth_prim *prims_dev, int32_t n_prims,
+                         const rf_pose *pose, double fx, double fy, double cx,
+                         double cy, int32_t width, int32_t height,
+                         const rf_synth_ref_params *params, double *depth_dev,
+                         void *stream);
+/* render_color (synth.py:253-267) of a (noisy) depth map: colour [h][w][3] */
+rf_status rf_synth_color(const rf_synth_prim *prims_dev, int32_t n_prims,
+                         const rf_pose *pose, double fx, double fy, double cx,
+                         double cy, int32_t width, int32_t height,
+                         const rf_synth_ref_params *params, const double *depth_dev,
+                         double *color_dev, void *stream);
+/* gaussian_filter(color, sigma=(s, s, 0)) in place (mode 'reflect',
+ * synth.py:353-355); tmp_dev: h*w*3 doubles of scratch */
+rf_status rf_synth_blur(double *color_dev, double *tmp_dev, int32_t width,
+                        int32_t height, const rf_synth_gauss *g, void *stream);
 
 #ifdef __cplusplus
 }

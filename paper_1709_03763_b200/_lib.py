@@ -139,18 +139,23 @@ class RfSynthPrim(ctypes.Structure):
     ]
 
 
-class RfSynthParams(ctypes.Structure):
+class RfSynthRefParams(ctypes.Structure):
     _fields_ = [
         ("z_max", ctypes.c_double),
         ("tol", ctypes.c_double),
-        ("sigma0", ctypes.c_double),
         ("ambient", ctypes.c_double),
         ("diffuse", ctypes.c_double),
-        ("light", ctypes.c_double * 3),
-        ("seed", ctypes.c_uint64),
+        ("neg_light", ctypes.c_double * 3),
+        ("normal_eps", ctypes.c_double),
         ("steps", ctypes.c_int32),
+        ("gemm_order", ctypes.c_int32),
+        ("gemv_order", ctypes.c_int32),
         ("_pad", ctypes.c_int32),
     ]
+
+
+class RfSynthGauss(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_double * 64), ("r", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 _vp = ctypes.c_void_p
@@ -242,8 +247,18 @@ SIGNATURES = {
     "rf_reserve": (_S, [_vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
     "rf_profile_begin": (_S, [_vp]),
     "rf_profile_end": (_S, [_vp, ctypes.POINTER(RfProfile)]),
-    "rf_synth_render": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4
-                        + [ctypes.c_int32] * 2 + [ctypes.POINTER(RfSynthParams), _vp, _vp, _vp]),
+    "rf_mesh_connect": (_S, [_vp, ctypes.POINTER(_vp), ctypes.c_int32]),
+    "rf_mesh_ipc_handle": (_S, [_vp, _vp]),
+    "rf_mesh_ipc_open": (_S, [_vp, _vp, c_int64_p]),
+    "rf_mesh_blocks": (_S, [_vp, c_int64_p, c_int64_p, c_int64_p, ctypes.c_int64,
+                            ctypes.POINTER(ctypes.c_int64)]),
+    "rf_synth_depth": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4
+                       + [ctypes.c_int32] * 2 + [ctypes.POINTER(RfSynthRefParams), _vp, _vp]),
+    "rf_synth_color": (_S, [_vp, ctypes.c_int32, ctypes.POINTER(RfPose)] + [ctypes.c_double] * 4
+                       + [ctypes.c_int32] * 2 + [ctypes.POINTER(RfSynthRefParams), _vp, _vp,
+                                                 _vp]),
+    "rf_synth_blur": (_S, [_vp, _vp, ctypes.c_int32, ctypes.c_int32,
+                           ctypes.POINTER(RfSynthGauss), _vp]),
 }
 
 _lib = None

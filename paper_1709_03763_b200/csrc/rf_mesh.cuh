@@ -113,10 +113,39 @@ __device__ __forceinline__ int mc_nb_index(int dx, int dy, int dz) {
   return map[code];
 }
 
-// The block's own slot and its seven +axis neighbours, looked up once per CTA.
-__device__ __forceinline__ void mc_neighbours(const Table& T, long long key, int slot, int* nb) {
+// Hash tables of the other shards of a hash-sharded volume (device
+// pointers valid here: the same device, or peers mapped over NVLink by
+// CUDA IPC).  Marching cubes borrows the +x / +y / +z neighbours of a block
+// (meshing.py:112-147); on a sharded volume a neighbour may live on another
+// shard, so its corners are read from that shard's pool directly.
+struct MeshPeer {
+  const int* heads;
+  const long long* keys;
+  const int* next;
+  const double* pool;
+  long long buckets;
+};
+struct MeshPeers {
+  MeshPeer p[kMaxShards];
+  int count;  // shards (1: every neighbour is local)
+  int self;
+};
+
+__device__ __forceinline__ int peer_find(const MeshPeer& P, long long key) {
+  int n = __ldcg(&P.heads[block_hash_of_key(key, P.buckets)]);
+  while (n >= 0) {
+    if (__ldcg(&P.keys[n]) == key) return n;
+    n = __ldcg(&P.next[n]);
+  }
+  return -1;
+}
+
+// The block itself and its seven +axis neighbours (block base pointers, null
+// when absent), looked up once per CTA.
+__device__ __forceinline__ void mc_neighbours(const Table& T, const MeshPeers& mp, long long key,
+                                              int slot, const double** nb) {
   if (threadIdx.x < 8) {
-    int s = slot;
+    const double* ptr = T.pool + static_cast<size_t>(slot) * kBlockDoubles;
     if (threadIdx.x > 0) {
       constexpr int off[8][3] = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}, {0, 0, 1},
                                  {1, 1, 0}, {1, 0, 1}, {0, 1, 1}, {1, 1, 1}};
@@ -126,13 +155,20 @@ __device__ __forceinline__ void mc_neighbours(const Table& T, long long key, int
       by += off[threadIdx.x][1];
       bz += off[threadIdx.x][2];
       const long long lim = kPackBias;  // packed coordinates must stay in 21 bits
-      s = -1;
+      ptr = nullptr;
       if (bx < lim && by < lim && bz < lim) {
         const long long k = pack_key(bx, by, bz);
-        s = chain_find(T, ld_acquire(&T.heads[block_hash_of_key(k, T.buckets)]), -1, k);
+        const int o = mp.count > 1 ? key_owner(k, mp.count) : mp.self;
+        if (o == mp.self) {
+          const int s = chain_find(T, ld_acquire(&T.heads[block_hash_of_key(k, T.buckets)]), -1, k);
+          if (s >= 0) ptr = T.pool + static_cast<size_t>(s) * kBlockDoubles;
+        } else {
+          const int s = peer_find(mp.p[o], k);
+          if (s >= 0) ptr = mp.p[o].pool + static_cast<size_t>(s) * kBlockDoubles;
+        }
       }
     }
-    nb[threadIdx.x] = s;
+    nb[threadIdx.x] = ptr;
   }
 }
 
@@ -142,21 +178,21 @@ constexpr int kMcPad = 9;        // padded corner grid (meshing.py:112-146)
 constexpr int kMcPadN = kMcPad * kMcPad * kMcPad;
 
 // Padded position (x, y, z) in 0..8: owning block (neighbour index) and voxel.
-__device__ __forceinline__ void mc_pad_source(const int* nb, int x, int y, int z, int& slot,
-                                              int& voxel) {
-  slot = nb[mc_nb_index(x >> 3, y >> 3, z >> 3)];
+__device__ __forceinline__ const double* mc_pad_source(const double* const* nb, int x, int y,
+                                                       int z, int& voxel) {
   voxel = (x & 7) + 8 * (y & 7) + 64 * (z & 7);
+  return nb[mc_nb_index(x >> 3, y >> 3, z >> 3)];
 }
 
 // Stage D and W of the 9x9x9 padded grid in shared memory (coalesced along
 // x; an absent neighbour's corners read as W = 0, unobserved).
-__device__ __forceinline__ void mc_stage(const Table& T, const int* nb, double* s_d, double* s_w) {
+__device__ __forceinline__ void mc_stage(const double* const* nb, double* s_d, double* s_w) {
   for (int j = threadIdx.x; j < kMcPadN; j += blockDim.x) {
-    int slot, voxel;
-    mc_pad_source(nb, j % kMcPad, (j / kMcPad) % kMcPad, j / (kMcPad * kMcPad), slot, voxel);
-    const double* blk = T.pool + static_cast<size_t>(slot < 0 ? 0 : slot) * kBlockDoubles;
-    s_d[j] = slot < 0 ? 0.0 : blk[voxel];
-    s_w[j] = slot < 0 ? 0.0 : blk[kBlockVoxels + voxel];
+    int voxel;
+    const double* blk =
+        mc_pad_source(nb, j % kMcPad, (j / kMcPad) % kMcPad, j / (kMcPad * kMcPad), voxel);
+    s_d[j] = blk ? blk[voxel] : 0.0;
+    s_w[j] = blk ? blk[kBlockVoxels + voxel] : 0.0;
   }
 }
 
@@ -182,16 +218,17 @@ __device__ __forceinline__ unsigned mc_case(const double* s_d, const double* s_w
 }
 
 // Pass 1: vertices and triangles per block (sorted order).
-__global__ void __launch_bounds__(kMcThreads, 8) k_mesh_count(Table T, const long long* keys,
+__global__ void __launch_bounds__(kMcThreads, 8) k_mesh_count(Table T, MeshPeers mp,
+                                                           const long long* keys,
                                                            const int* slots, long long n,
                                                            long long* nv, long long* nt) {
-  __shared__ int nb[8];
+  __shared__ const double* nb[8];
   __shared__ double s_d[kMcPadN], s_w[kMcPadN];
   __shared__ int s_v[kMcThreads / 32], s_t[kMcThreads / 32];
   for (long long b = blockIdx.x; b < n; b += gridDim.x) {
-    mc_neighbours(T, keys[b], slots[b], nb);
+    mc_neighbours(T, mp, keys[b], slots[b], nb);
     __syncthreads();
-    mc_stage(T, nb, s_d, s_w);
+    mc_stage(nb, s_d, s_w);
     __syncthreads();
     int v = 0, t = 0;
 #pragma unroll
@@ -228,13 +265,14 @@ __global__ void __launch_bounds__(kMcThreads, 8) k_mesh_count(Table T, const lon
 // live cell lists its (cell, cut edge) and (cell, triangle) entries in shared
 // memory at its prefix; the CTA then writes the block's contiguous output
 // ranges one vertex / triangle per thread (coalesced stores).
-__global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, const long long* keys,
+__global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, MeshPeers mp,
+                                                          const long long* keys,
                                                           const int* slots, long long n,
                                                           const long long* v_off,
                                                           const long long* t_off, double vs,
                                                           double* verts, double* cols,
                                                           long long* tris) {
-  __shared__ int nb[8];
+  __shared__ const double* nb[8];
   __shared__ double s_d[kMcPadN], s_w[kMcPadN];
   __shared__ unsigned short s_vlist[kBlockVoxels * 12];  // cell << 4 | edge
   __shared__ unsigned short s_tlist[kBlockVoxels * 5];   // cell << 3 | triangle
@@ -244,9 +282,9 @@ __global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, const long
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (long long b = blockIdx.x; b < n; b += gridDim.x) {
     const long long key = keys[b];
-    mc_neighbours(T, key, slots[b], nb);
+    mc_neighbours(T, mp, key, slots[b], nb);
     __syncthreads();
-    mc_stage(T, nb, s_d, s_w);
+    mc_stage(nb, s_d, s_w);
     __syncthreads();
     // this thread's cells l0 .. l0 + kMcCells - 1 (consecutive: l order)
     const int l0 = threadIdx.x * kMcCells;
@@ -317,11 +355,11 @@ __global__ void __launch_bounds__(kMcThreads, 6) k_mesh_emit(Table T, const long
       const double base[3] = {(static_cast<double>(x + bx * kBlockSide) + 0.5) * vs,
                               (static_cast<double>(y + by * kBlockSide) + 0.5) * vs,
                               (static_cast<double>(z + bz * kBlockSide) + 0.5) * vs};
-      int sa, va, sc, vc;
-      mc_pad_source(nb, x + kMcCorner[a][0], y + kMcCorner[a][1], z + kMcCorner[a][2], sa, va);
-      mc_pad_source(nb, x + kMcCorner[c][0], y + kMcCorner[c][1], z + kMcCorner[c][2], sc, vc);
-      const double* pa_blk = T.pool + static_cast<size_t>(sa) * kBlockDoubles;
-      const double* pc_blk = T.pool + static_cast<size_t>(sc) * kBlockDoubles;
+      int va, vc;  // both corners observed: their blocks exist
+      const double* pa_blk =
+          mc_pad_source(nb, x + kMcCorner[a][0], y + kMcCorner[a][1], z + kMcCorner[a][2], va);
+      const double* pc_blk =
+          mc_pad_source(nb, x + kMcCorner[c][0], y + kMcCorner[c][1], z + kMcCorner[c][2], vc);
       const long long vi = vb + j;
 #pragma unroll
       for (int k = 0; k < 3; ++k) {

@@ -1,14 +1,10 @@
-// rf_synth.cu -- measurement infrastructure: analytic-scene RGB-D renderer.
-//
-// Device counterpart of the reference's synthetic data generator
-// (/root/reference/pkg/src/refusion/synth.py:46-283): unions of signed
-// distance primitives (sphere, solid box, hollow room shell), sphere-traced
-// z-depth with 256 steps / 1e-5 tolerance, flat-albedo Lambert colour and
-// sigma0 * z^2 depth noise.  The CPU renderer takes 2.46 s per 640x480
-// frame, which rules out the 2,000-20,000-frame configs; this
-// kernel renders a frame in well under a millisecond.  It is NOT on the
-// timed hot path and makes no bit-parity claim with synth.py (its noise
-// stream is a counter-based hash, not numpy's PCG64).
+// rf_synth.cu -- the reference's synthetic RGB-D generator on the device
+// (/root/reference/pkg/src/refusion/synth.py:46-283): unions of
+// signed-distance primitives (sphere, solid box, hollow room shell),
+// sphere-traced z-depth (256 steps, 1e-5 tolerance) and flat-albedo Lambert
+// colour, evaluated in numpy's order so every pixel is bit-identical to the
+// reference's; the reference's 2.46 s per 640x480 frame becomes well under
+// a millisecond.  Measurement infrastructure, not the timed hot path.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -20,25 +16,59 @@ namespace {
 
 constexpr int kSphere = 0, kRoom = 2;  // kind 1 = BoxSolid
 
-__device__ __forceinline__ double prim_sdf(const rf_synth_prim& p, double x, double y, double z) {
+// ---------------------------------------------------------------------------
+// Faithful port: the reference's render_depth / render_color
+// (synth.py:220-267) evaluated in numpy's order, every double op rounded
+// individually (-fmad=false) -- bit-identical to the reference's arrays.
+//   * np.linalg.norm over the last axis of length 3: sqrt((a*a + b*b) + c*c)
+//   * np.maximum(a, b): a >= b || isnan(a) ? a : b;  np.minimum likewise
+//   * (n,3) @ (3,3) and (n,3) @ (3,): the host BLAS's multiply-add order,
+//     calibrated on the host (synth.detect_render_orders) like
+//     keyframe_fusion.detect_blas_order
+//   * sphere tracing: every alive ray adds max(s, 0) to t -- a converged ray
+//     included -- then leaves when converged or t > t_cap (synth.py:236-243)
+// The depth noise (numpy's PCG64 + ziggurat stream) is drawn on the host by
+// the same numpy call (synth.add_noise); the colour pass shades the noisy
+// depth, as make_sequence does (synth.py:348-352).
+
+__device__ __forceinline__ double np_max(double a, double b) { return (a >= b || isnan(a)) ? a : b; }
+__device__ __forceinline__ double np_min(double a, double b) { return (a <= b || isnan(a)) ? a : b; }
+
+__device__ __forceinline__ double np_norm3(double a, double b, double c) {
+  return sqrt((a * a + b * b) + c * c);
+}
+
+__device__ __forceinline__ double ref_row(const double* r, double p0, double p1, double p2,
+                                          int order) {
+  switch (order) {
+    case RF_BLAS_FMA_210: return fma(p2, r[2], fma(p1, r[1], p0 * r[0]));
+    case RF_BLAS_FMA_012: return fma(p0, r[0], fma(p1, r[1], p2 * r[2]));
+    case RF_BLAS_FMA_201: return fma(p2, r[2], fma(p0, r[0], p1 * r[1]));
+    default: return (p0 * r[0] + p1 * r[1]) + p2 * r[2];
+  }
+}
+
+// Sphere.sdf / BoxSolid.sdf / RoomShell.sdf (synth.py:46-81)
+__device__ __forceinline__ double ref_prim_sdf(const rf_synth_prim& p, double x, double y,
+                                               double z) {
   const double dx = x - p.center[0], dy = y - p.center[1], dz = z - p.center[2];
-  if (p.kind == kSphere) return sqrt(dx * dx + dy * dy + dz * dz) - p.size[0];
-  // box / room: synth.py:62-81
+  if (p.kind == kSphere) return np_norm3(dx, dy, dz) - p.size[0];
   const double qx = fabs(dx) - p.size[0], qy = fabs(dy) - p.size[1], qz = fabs(dz) - p.size[2];
-  const double ox = fmax(qx, 0.0), oy = fmax(qy, 0.0), oz = fmax(qz, 0.0);
-  const double outside = sqrt(ox * ox + oy * oy + oz * oz);
-  const double inside = fmin(fmax(qx, fmax(qy, qz)), 0.0);
+  const double outside = np_norm3(np_max(qx, 0.0), np_max(qy, 0.0), np_max(qz, 0.0));
+  const double inside = np_min(np_max(np_max(qx, qy), qz), 0.0);
   const double s = outside + inside;
   return p.kind == kRoom ? -s : s;
 }
 
-__device__ __forceinline__ double scene_sdf(const rf_synth_prim* prims, int n, double x, double y,
-                                            double z, int* which) {
-  double best = 1e300;
+// AnalyticScene.sdf (min over the stacked fields) and albedo_at's argmin
+// (first minimum), synth.py:91-101
+__device__ __forceinline__ double ref_scene_sdf(const rf_synth_prim* prims, int n, double x,
+                                                double y, double z, int* which) {
+  double best = ref_prim_sdf(prims[0], x, y, z);
   int arg = 0;
-  for (int i = 0; i < n; ++i) {
-    const double s = prim_sdf(prims[i], x, y, z);
-    if (s < best) {
+  for (int i = 1; i < n; ++i) {
+    const double s = ref_prim_sdf(prims[i], x, y, z);
+    if (s < best || (isnan(s) && !isnan(best))) {
       best = s;
       arg = i;
     }
@@ -47,105 +77,166 @@ __device__ __forceinline__ double scene_sdf(const rf_synth_prim* prims, int n, d
   return best;
 }
 
-__device__ __forceinline__ uint64_t mix(uint64_t z) {
-  z += 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-
-__device__ __forceinline__ double gauss(uint64_t seed, uint64_t idx) {
-  const uint64_t a = mix(seed ^ mix(idx * 2 + 1));
-  const uint64_t b = mix(seed ^ mix(idx * 2 + 2));
-  const double u1 = (static_cast<double>(a >> 11) + 1.0) * (1.0 / 9007199254740993.0);
-  const double u2 = static_cast<double>(b >> 11) * (1.0 / 9007199254740992.0);
-  return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
-}
-
-__global__ void k_render(const rf_synth_prim* __restrict__ prims_g, int n_prims, rf_pose pose,
-                         double fx, double fy, double cx, double cy, int width, int height,
-                         rf_synth_params sp, double* depth_out, double* color_out) {
+__global__ void k_render_depth_ref(const rf_synth_prim* __restrict__ prims_g, int n_prims,
+                                   rf_pose pose, double fx, double fy, double cx, double cy,
+                                   int width, int height, rf_synth_ref_params sp,
+                                   double* __restrict__ depth_out) {
   __shared__ rf_synth_prim prims[32];
-  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < n_prims && i < 32;
-       i += blockDim.x * blockDim.y)
+  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < n_prims; i += blockDim.x * blockDim.y)
+    prims[i] = prims_g[i];
+  __syncthreads();
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= width || v >= height) return;
+  // ray_grid (geometry.py:266-275), d_cam / norms (synth.py:223-226)
+  const double rx = (static_cast<double>(u) - cx) / fx;
+  const double ry = (static_cast<double>(v) - cy) / fy;
+  const double nrm = np_norm3(rx, ry, 1.0);
+  const double d0 = rx / nrm, d1 = ry / nrm, d2 = 1.0 / nrm;
+  const double* R = pose.R;  // d_world = d_cam @ R.T
+  const double w0 = ref_row(R + 0, d0, d1, d2, sp.gemm_order);
+  const double w1 = ref_row(R + 3, d0, d1, d2, sp.gemm_order);
+  const double w2 = ref_row(R + 6, d0, d1, d2, sp.gemm_order);
+  const double t_cap = sp.z_max * nrm;
+  double t = 0.0;
+  bool hit = false;
+  for (int s = 0; s < sp.steps; ++s) {  // synth.py:236-243
+    const double sd = ref_scene_sdf(prims, n_prims, pose.t[0] + t * w0, pose.t[1] + t * w1,
+                                    pose.t[2] + t * w2, nullptr);
+    const bool conv = sd < sp.tol;
+    hit = hit || conv;
+    t = t + np_max(sd, 0.0);
+    if (conv || !(t <= t_cap)) break;
+  }
+  double depth = hit ? t * d2 : 0.0;  // synth.py:245-248
+  if (depth > sp.z_max) depth = 0.0;
+  depth_out[static_cast<size_t>(v) * width + u] = depth;
+}
+
+__global__ void k_render_color_ref(const rf_synth_prim* __restrict__ prims_g, int n_prims,
+                                   rf_pose pose, double fx, double fy, double cx, double cy,
+                                   int width, int height, rf_synth_ref_params sp,
+                                   const double* __restrict__ depth, double* __restrict__ color) {
+  __shared__ rf_synth_prim prims[32];
+  for (int i = threadIdx.x + threadIdx.y * blockDim.x; i < n_prims; i += blockDim.x * blockDim.y)
     prims[i] = prims_g[i];
   __syncthreads();
   const int u = blockIdx.x * blockDim.x + threadIdx.x;
   const int v = blockIdx.y * blockDim.y + threadIdx.y;
   if (u >= width || v >= height) return;
   const size_t pix = static_cast<size_t>(v) * width + u;
-  // synth.py:220-250
-  double dcx = (u - cx) / fx, dcy = (v - cy) / fy, dcz = 1.0;
-  const double nrm = sqrt(dcx * dcx + dcy * dcy + dcz * dcz);
-  dcx /= nrm;
-  dcy /= nrm;
-  dcz /= nrm;
-  const double* R = pose.R;
-  const double dwx = R[0] * dcx + R[1] * dcy + R[2] * dcz;
-  const double dwy = R[3] * dcx + R[4] * dcy + R[5] * dcz;
-  const double dwz = R[6] * dcx + R[7] * dcy + R[8] * dcz;
-  const double t_cap = sp.z_max * nrm;
-  double t = 0.0;
-  bool hit = false;
-  for (int s = 0; s < sp.steps; ++s) {
-    const double d = scene_sdf(prims, n_prims, pose.t[0] + t * dwx, pose.t[1] + t * dwy,
-                               pose.t[2] + t * dwz, nullptr);
-    if (d < sp.tol) {
-      hit = true;
-      break;
-    }
-    t += fmax(d, 0.0);
-    if (t > t_cap) break;
-  }
-  double depth = hit ? t * dcz : 0.0;
-  if (depth > sp.z_max) depth = 0.0;
-  const double clean = depth;
-  if (depth > 0.0 && sp.sigma0 > 0.0) {  // synth.py:270-283
-    depth = fmax(depth + gauss(sp.seed, pix) * sp.sigma0 * depth * depth, 0.0);
-  }
-  depth_out[pix] = depth;
-  if (!color_out) return;
+  const double z = depth[pix];
   double c0 = 0.0, c1 = 0.0, c2 = 0.0;
-  if (clean > 0.0) {  // synth.py:253-267 (shaded at the noiseless hit point)
-    const double px = pose.t[0] + t * dwx, py = pose.t[1] + t * dwy, pz = pose.t[2] + t * dwz;
+  if (z > 0.0) {  // synth.py:253-267
+    const double rx = (static_cast<double>(u) - cx) / fx;
+    const double ry = (static_cast<double>(v) - cy) / fy;
+    const double q0 = rx * z, q1 = ry * z;
+    const double* R = pose.R;  // p_cam @ R.T + t
+    const double px = ref_row(R + 0, q0, q1, z, sp.gemm_order) + pose.t[0];
+    const double py = ref_row(R + 3, q0, q1, z, sp.gemm_order) + pose.t[1];
+    const double pz = ref_row(R + 6, q0, q1, z, sp.gemm_order) + pose.t[2];
     int which = 0;
-    scene_sdf(prims, n_prims, px, py, pz, &which);
-    const double e = 1e-4;
-    double nx = scene_sdf(prims, n_prims, px + e, py, pz, nullptr) -
-                scene_sdf(prims, n_prims, px - e, py, pz, nullptr);
-    double ny = scene_sdf(prims, n_prims, px, py + e, pz, nullptr) -
-                scene_sdf(prims, n_prims, px, py - e, pz, nullptr);
-    double nz = scene_sdf(prims, n_prims, px, py, pz + e, nullptr) -
-                scene_sdf(prims, n_prims, px, py, pz - e, nullptr);
-    double nn = sqrt(nx * nx + ny * ny + nz * nz);
+    ref_scene_sdf(prims, n_prims, px, py, pz, &which);
+    // normal_at (synth.py:103-112): points +/- step, step = eps on one axis
+    const double e = sp.normal_eps;
+    double n0 = ref_scene_sdf(prims, n_prims, px + e, py + 0.0, pz + 0.0, nullptr) -
+                ref_scene_sdf(prims, n_prims, px - e, py - 0.0, pz - 0.0, nullptr);
+    double n1 = ref_scene_sdf(prims, n_prims, px + 0.0, py + e, pz + 0.0, nullptr) -
+                ref_scene_sdf(prims, n_prims, px - 0.0, py - e, pz - 0.0, nullptr);
+    double n2 = ref_scene_sdf(prims, n_prims, px + 0.0, py + 0.0, pz + e, nullptr) -
+                ref_scene_sdf(prims, n_prims, px - 0.0, py - 0.0, pz - e, nullptr);
+    double nn = np_norm3(n0, n1, n2);
     if (nn == 0.0) nn = 1.0;
-    nx /= nn;
-    ny /= nn;
-    nz /= nn;
-    const double lam = sp.ambient + sp.diffuse * fmax(0.0, -(nx * sp.light[0] + ny * sp.light[1] +
-                                                             nz * sp.light[2]));
-    c0 = fmin(fmax(prims[which].albedo[0] * lam, 0.0), 255.0);
-    c1 = fmin(fmax(prims[which].albedo[1] * lam, 0.0), 255.0);
-    c2 = fmin(fmax(prims[which].albedo[2] * lam, 0.0), 255.0);
+    n0 = n0 / nn;
+    n1 = n1 / nn;
+    n2 = n2 / nn;
+    const double dot = ref_row(sp.neg_light, n0, n1, n2, sp.gemv_order);  // normal @ (-L)
+    const double lam = sp.ambient + sp.diffuse * np_max(0.0, dot);
+    const double* a = prims[which].albedo;
+    c0 = np_min(np_max(a[0] * lam, 0.0), 255.0);  // np.clip
+    c1 = np_min(np_max(a[1] * lam, 0.0), 255.0);
+    c2 = np_min(np_max(a[2] * lam, 0.0), 255.0);
   }
-  color_out[3 * pix] = c0;
-  color_out[3 * pix + 1] = c1;
-  color_out[3 * pix + 2] = c2;
+  color[3 * pix] = c0;
+  color[3 * pix + 1] = c1;
+  color[3 * pix + 2] = c2;
+}
+
+// scipy.ndimage.correlate1d with a symmetric kernel, mode 'reflect'
+// (d c b a | a b c d | d c b a), along one axis of an (h, w, 3) image:
+// out = x0*w0 + sum_{j=r..1} (x[-j] + x[+j]) * w[j] -- the loop order of
+// scipy's symmetric branch (the unsharp mask's k_gauss_* use 'nearest').
+__device__ __forceinline__ int reflect_idx(int i, int len) {
+  if (len == 1) return 0;
+  const int period = 2 * len;
+  i %= period;
+  if (i < 0) i += period;
+  return i < len ? i : period - 1 - i;
+}
+
+__global__ void k_blur_reflect(const double* __restrict__ in, int W, int H, int axis,
+                               rf_synth_gauss g, double* __restrict__ out) {
+  const int u = blockIdx.x * blockDim.x + threadIdx.x;
+  const int v = blockIdx.y * blockDim.y + threadIdx.y;
+  if (u >= W || v >= H) return;
+  const int len = axis == 0 ? H : W;
+  const int pos = axis == 0 ? v : u;
+  auto at = [&](int i, int ch) {
+    const int j = reflect_idx(i, len);
+    const size_t q = axis == 0 ? static_cast<size_t>(j) * W + u : static_cast<size_t>(v) * W + j;
+    return in[3 * q + ch];
+  };
+  const size_t pix = static_cast<size_t>(v) * W + u;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = in[3 * pix + ch] * g.w[0];
+    for (int j = g.r; j >= 1; --j) acc = acc + (at(pos - j, ch) + at(pos + j, ch)) * g.w[j];
+    out[3 * pix + ch] = acc;
+  }
 }
 
 }  // namespace
 
-extern "C" rf_status rf_synth_render(const rf_synth_prim* prims_dev, int32_t n_prims,
-                                     const rf_pose* pose, double fx, double fy, double cx,
-                                     double cy, int32_t width, int32_t height,
-                                     const rf_synth_params* params, double* depth_dev,
-                                     double* color_dev, void* stream) {
+extern "C" rf_status rf_synth_depth(const rf_synth_prim* prims_dev, int32_t n_prims,
+                                    const rf_pose* pose, double fx, double fy, double cx,
+                                    double cy, int32_t width, int32_t height,
+                                    const rf_synth_ref_params* params, double* depth_dev,
+                                    void* stream) {
   if (!prims_dev || n_prims <= 0 || n_prims > 32 || !pose || !params || !depth_dev ||
-      width <= 0 || height <= 0)
+      width <= 0 || height <= 0 || params->steps < 0)
     return RF_INVALID_ARG;
   dim3 block(16, 8);
   dim3 grid((width + 15) / 16, (height + 7) / 8);
-  k_render<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+  k_render_depth_ref<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
+      prims_dev, n_prims, *pose, fx, fy, cx, cy, width, height, *params, depth_dev);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+extern "C" rf_status rf_synth_color(const rf_synth_prim* prims_dev, int32_t n_prims,
+                                    const rf_pose* pose, double fx, double fy, double cx,
+                                    double cy, int32_t width, int32_t height,
+                                    const rf_synth_ref_params* params, const double* depth_dev,
+                                    double* color_dev, void* stream) {
+  if (!prims_dev || n_prims <= 0 || n_prims > 32 || !pose || !params || !depth_dev ||
+      !color_dev || width <= 0 || height <= 0)
+    return RF_INVALID_ARG;
+  dim3 block(16, 8);
+  dim3 grid((width + 15) / 16, (height + 7) / 8);
+  k_render_color_ref<<<grid, block, 0, static_cast<cudaStream_t>(stream)>>>(
       prims_dev, n_prims, *pose, fx, fy, cx, cy, width, height, *params, depth_dev, color_dev);
+  return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
+}
+
+extern "C" rf_status rf_synth_blur(double* color_dev, double* tmp_dev, int32_t width,
+                                   int32_t height, const rf_synth_gauss* g, void* stream) {
+  if (!color_dev || !tmp_dev || !g || width <= 0 || height <= 0 || g->r < 0 || g->r > 63)
+    return RF_INVALID_ARG;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  dim3 block(32, 8);
+  dim3 grid((width + 31) / 32, (height + 7) / 8);
+  // gaussian_filter(color, (sigma, sigma, 0)): axis 0, then axis 1 (the
+  // channel axis has sigma 0 and is skipped, scipy _filters.py)
+  k_blur_reflect<<<grid, block, 0, s>>>(color_dev, width, height, 0, *g, tmp_dev);
+  k_blur_reflect<<<grid, block, 0, s>>>(tmp_dev, width, height, 1, *g, color_dev);
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }

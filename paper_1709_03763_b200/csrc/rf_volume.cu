@@ -98,6 +98,7 @@ struct rf_volume {
   int n_sms = 148;
   int fuse_grid = 148 * 2;
   int fuse_grids[4] = {148, 148, 148, 148};  // per FuseMode, n_sms x occupancy
+  int check_grid = 148;                       // k_check: n_sms x occupancy
   // staging of host keyframe planes (rf_kf_view.planes_on_host)
   struct StageSlot {
     double* buf = nullptr;
@@ -142,6 +143,10 @@ struct rf_volume {
   SyncSlot* sync_own = nullptr;
   SyncSlot* sync_peer[kMaxShards] = {};
   bool sync_ipc[kMaxShards] = {};
+  // the other shards' hash tables for marching cubes' cross-shard neighbours
+  // (rf_mesh_connect / rf_mesh_ipc_open); count 1 = not connected
+  MeshPeers mesh{};
+  void* mesh_ipc[kMaxShards][4] = {};
   int sync_max_ops = 0;
   bool sync_on = false;
   unsigned sync_gen = 0;
@@ -566,6 +571,9 @@ constexpr size_t kFuseDynSmem = static_cast<size_t>(kFuseThreads / 32) * kTileWa
 // Launch the batched fuse kernel of mode kMode.
 template <int kMode>
 void launch_fuse(rf_volume* v, const FuseParams& p) {
+  if constexpr (kMode == kCheckRemove) {  // the de-integration check: its own lean kernel
+    launch(k_check, v->check_grid, kFuseThreads, 0, v->stream, v->T, p);
+  } else {
 #if RF_KF_TMA
   CUtensorMap md, mw;
   FuseParams q = p;
@@ -576,6 +584,7 @@ void launch_fuse(rf_volume* v, const FuseParams& p) {
 #else
   launch(k_fuse<kMode>, v->fuse_grids[kMode], kFuseThreads, 0, v->stream, v->T, p);
 #endif
+  }
 }
 
 // Host keyframe planes (planes_on_host): copy each distinct keyframe of a
@@ -946,17 +955,20 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
 #if RF_KF_TMA
   const size_t dsm = kFuseDynSmem;
   cudaFuncSetAttribute(k_fuse<kIntegrate>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
-  cudaFuncSetAttribute(k_fuse<kCheckRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
   cudaFuncSetAttribute(k_fuse<kApplyRemove>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
   cudaFuncSetAttribute(k_fuse<kRemoveReadd>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm));
 #else
   const size_t dsm = 0;
 #endif
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[0], k_fuse<kIntegrate>, kFuseThreads, dsm);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[1], k_fuse<kCheckRemove>, kFuseThreads, dsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[2], k_fuse<kApplyRemove>, kFuseThreads, dsm);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[3], k_fuse<kRemoveReadd>, kFuseThreads, dsm);
   for (int m = 0; m < 4; ++m) v->fuse_grids[m] = v->n_sms * std::max(occ[m], 1);
+  {
+    int oc = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, k_check, kFuseThreads, 0);
+    v->check_grid = v->n_sms * std::max(oc, 1);
+  }
   v->fuse_grid = v->fuse_grids[0];
   v->fp_grid_cap = v->n_sms * 8;
   const size_t cap = static_cast<size_t>(cfg->block_capacity);
@@ -1041,6 +1053,8 @@ rf_status rf_volume_destroy(rf_volume* v) {
   for (int s = 0; s < kMaxShards; ++s) {
     if (v->route_ipc[s]) cudaIpcCloseMemHandle(v->route_peer[s]);
     if (v->sync_ipc[s]) cudaIpcCloseMemHandle(v->sync_peer[s]);
+    for (int a = 0; a < 4; ++a)
+      if (v->mesh_ipc[s][a]) cudaIpcCloseMemHandle(v->mesh_ipc[s][a]);
   }
   if (v->route_own) cudaFree(v->route_own);
   if (v->sync_own) cudaFree(v->sync_own);
@@ -1731,6 +1745,17 @@ rf_status weld_device(rf_volume* v, double tol, double*& dv, double*& dc, long l
 }
 
 // marching_cubes (+ optional device weld when tol > 0) into host arrays.
+// The peer tables marching cubes reads cross-shard neighbours from: every
+// shard once connected (own entry = this table), else this table alone.
+MeshPeers mesh_peers_of(const rf_volume* v) {
+  MeshPeers mp = v->mesh;
+  if (mp.count < 2) {
+    mp.count = 1;
+    mp.self = 0;
+  }
+  return mp;
+}
+
 rf_status mesh_to_host(rf_volume* v, double tol, double* vertices, double* colors,
                        int64_t* triangles, int64_t vcap, int64_t tcap, int64_t* nv_out,
                        int64_t* nt_out) {
@@ -1773,7 +1798,7 @@ rf_status mesh_to_host(rf_volume* v, double tol, double* vertices, double* color
   long long* nt = cnt + (n + 1);
   cudaMemsetAsync(cnt, 0, sizeof(long long) * 2 * (n + 1), st);
   const int grid = static_cast<int>(std::min<long long>(n, 1LL << 20));
-  k_mesh_count<<<grid, kMcThreads, 0, st>>>(v->T, keys_sorted, slots_sorted, n, nv, nt);
+  k_mesh_count<<<grid, kMcThreads, 0, st>>>(v->T, mesh_peers_of(v), keys_sorted, slots_sorted, n, nv, nt);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_scan, nv, off, static_cast<int>(n + 1), st);
   cub::DeviceScan::ExclusiveSum(tmp, tmp_scan, nt, off + (n + 1), static_cast<int>(n + 1), st);
   long long tot[2] = {0, 0};
@@ -1793,7 +1818,7 @@ rf_status mesh_to_host(rf_volume* v, double tol, double* vertices, double* color
         cudaMallocAsync(&dt, sizeof(long long) * 3 * std::max(tot[1], 1LL), st) != cudaSuccess) {
       rs = RF_CAPACITY;
     } else {
-      k_mesh_emit<<<grid, kMcThreads, 0, st>>>(v->T, keys_sorted, slots_sorted, n, off,
+      k_mesh_emit<<<grid, kMcThreads, 0, st>>>(v->T, mesh_peers_of(v), keys_sorted, slots_sorted, n, off,
                                                off + (n + 1), v->cfg.voxel_size, dv, dc, dt);
       long long mv = tot[0], mt = tot[1];
       if (tol > 0.0) {
@@ -2109,6 +2134,120 @@ rf_status rf_profile_end(rf_volume* v, rf_profile* out) {
   v->profiling = false;
   *out = p;
   return RF_OK;
+}
+
+}  // extern "C"
+
+// ---- cross-shard marching cubes --------------------------------
+
+extern "C" {
+
+rf_status rf_mesh_connect(rf_volume* v, rf_volume* const* shards, int32_t count) {
+  if (!v || !shards || count != v->cfg.shard_count || count < 2 || count > kMaxShards)
+    return RF_INVALID_ARG;
+  if (shards[v->cfg.shard_rank] != v)
+    return fail(v, RF_INVALID_ARG, "rf_mesh_connect: own entry mismatch");
+  MeshPeers mp{};
+  for (int s = 0; s < count; ++s) {
+    const rf_volume* o = shards[s];
+    if (!o || o->cfg.shard_count != count || o->cfg.shard_rank != s) return RF_INVALID_ARG;
+    mp.p[s] = MeshPeer{o->T.heads, o->T.keys, o->T.next, o->T.pool, o->T.buckets};
+  }
+  mp.count = count;
+  mp.self = v->cfg.shard_rank;
+  v->mesh = mp;
+  return RF_OK;
+}
+
+rf_status rf_mesh_ipc_handle(rf_volume* v, void* handles) {
+  if (!v || !handles) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  const void* arr[4] = {v->T.heads, v->T.keys, v->T.next, v->T.pool};
+  for (int a = 0; a < 4; ++a) {
+    cudaIpcMemHandle_t h;
+    RF_CUDA_TRY(v, cudaIpcGetMemHandle(&h, const_cast<void*>(arr[a])));
+    std::memcpy(static_cast<char*>(handles) + a * sizeof(h), &h, sizeof(h));
+  }
+  return RF_OK;
+}
+
+rf_status rf_mesh_ipc_open(rf_volume* v, const void* handles, const int64_t* buckets) {
+  if (!v || !handles || !buckets || v->cfg.shard_count < 2) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  const int G = v->cfg.shard_count;
+  MeshPeers mp{};
+  for (int s = 0; s < G; ++s) {
+    if (s == v->cfg.shard_rank) {
+      mp.p[s] = MeshPeer{v->T.heads, v->T.keys, v->T.next, v->T.pool, v->T.buckets};
+      continue;
+    }
+    void* ptr[4] = {};
+    for (int a = 0; a < 4; ++a) {
+      if (v->mesh_ipc[s][a]) {
+        ptr[a] = v->mesh_ipc[s][a];
+        continue;
+      }
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, static_cast<const char*>(handles) + (4 * s + a) * sizeof(h), sizeof(h));
+      RF_CUDA_TRY(v, cudaIpcOpenMemHandle(&ptr[a], h, cudaIpcMemLazyEnablePeerAccess));
+      v->mesh_ipc[s][a] = ptr[a];
+    }
+    mp.p[s] = MeshPeer{static_cast<const int*>(ptr[0]), static_cast<const long long*>(ptr[1]),
+                       static_cast<const int*>(ptr[2]), static_cast<const double*>(ptr[3]),
+                       static_cast<long long>(buckets[s])};
+  }
+  mp.count = G;
+  mp.self = v->cfg.shard_rank;
+  v->mesh = mp;
+  return RF_OK;
+}
+
+rf_status rf_mesh_blocks(rf_volume* v, int64_t* keys, int64_t* vcounts, int64_t* tcounts,
+                         int64_t cap, int64_t* n_out) {
+  if (!v || !n_out || cap < 0) return RF_INVALID_ARG;
+  cudaSetDevice(v->cfg.device);
+  cudaStream_t st = v->stream;
+  int* d_list = nullptr;
+  RF_CUDA_TRY(v, cudaMallocAsync(&d_list, sizeof(int) * v->T.capacity, st));
+  cudaMemsetAsync(v->d_u64, 0, sizeof(unsigned long long), st);
+  k_list_live<<<v->n_sms * 4, 256, 0, st>>>(v->T, d_list, v->d_u64);
+  cudaMemcpyAsync(v->h_u64, v->d_u64, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  const long long n = static_cast<long long>(v->h_u64[0]);
+  *n_out = n;
+  rf_status rs = RF_OK;
+  if (n > 0 && keys && vcounts && tcounts && n <= cap) {
+    long long *dk = nullptr, *dks = nullptr, *cnt = nullptr;
+    int* slots_sorted = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_sort = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_sort, dk, dks, d_list, slots_sorted,
+                                    static_cast<int>(n), 0, 63, st);
+    if (cudaMallocAsync(&dk, sizeof(long long) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&dks, sizeof(long long) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&slots_sorted, sizeof(int) * n, st) != cudaSuccess ||
+        cudaMallocAsync(&cnt, sizeof(long long) * 2 * n, st) != cudaSuccess ||
+        cudaMallocAsync(&tmp, std::max<size_t>(tmp_sort, 1), st) != cudaSuccess) {
+      rs = RF_CAPACITY;
+    } else {
+      k_gather_keys<<<static_cast<int>((n + 255) / 256), 256, 0, st>>>(v->T, d_list, n, dk);
+      cub::DeviceRadixSort::SortPairs(tmp, tmp_sort, dk, dks, d_list, slots_sorted,
+                                      static_cast<int>(n), 0, 63, st);
+      cudaMemsetAsync(cnt, 0, sizeof(long long) * 2 * n, st);
+      const int grid = static_cast<int>(std::min<long long>(n, 1LL << 20));
+      k_mesh_count<<<grid, kMcThreads, 0, st>>>(v->T, mesh_peers_of(v), dks, slots_sorted, n,
+                                                cnt, cnt + n);
+      cudaMemcpyAsync(keys, dks, sizeof(long long) * n, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(vcounts, cnt, sizeof(long long) * n, cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(tcounts, cnt + n, sizeof(long long) * n, cudaMemcpyDeviceToHost, st);
+    }
+    for (void* b : {static_cast<void*>(dk), static_cast<void*>(dks),
+                    static_cast<void*>(slots_sorted), static_cast<void*>(cnt), tmp})
+      if (b) cudaFreeAsync(b, st);
+  }
+  cudaFreeAsync(d_list, st);
+  RF_CUDA_TRY(v, cudaStreamSynchronize(st));
+  return rs;
 }
 
 }  // extern "C"

@@ -154,6 +154,46 @@ def rotation_angle(R):
     return 0.0 if angle < 1e-12 else angle
 
 
+def rotation_from_axis_angle(axis, angle):
+    """Rodrigues rotation about a (not necessarily unit) axis
+    (reference geometry.py:177-185, same expressions)."""
+    axis = np.asarray(axis, dtype=np.float64)
+    n = np.linalg.norm(axis)
+    if n == 0 or angle == 0:
+        return np.eye(3)
+    x, y, z = axis / n
+    K = np.array([[0, -z, y], [z, 0, -x], [-y, x, 0]])
+    return np.eye(3) + np.sin(angle) * K + (1 - np.cos(angle)) * (K @ K)
+
+
+def axis_angle_from_rotation(R):
+    """Inverse of Rodrigues: (unit axis, angle in [0, pi])
+    (reference geometry.py:188-204, same expressions)."""
+    cos_a = min(1.0, max(-1.0, (np.trace(R) - 1.0) / 2.0))
+    angle = float(np.arccos(cos_a))
+    if angle < 1e-12:
+        return np.array([1.0, 0.0, 0.0]), 0.0
+    if np.pi - angle < 1e-6:
+        M = (R + np.eye(3)) / 2.0
+        axis = np.sqrt(np.maximum(np.diag(M), 0.0))
+        k = int(np.argmax(axis))
+        if axis[k] > 0:
+            axis = M[:, k] / axis[k]
+        return axis / np.linalg.norm(axis), angle
+    v = np.array([R[2, 1] - R[1, 2], R[0, 2] - R[2, 0], R[1, 0] - R[0, 1]])
+    return v / (2.0 * np.sin(angle)), angle
+
+
+def pose_interpolate(T, U, t):
+    """Geodesic interpolation T (t=0) -> U (t=1) (reference
+    geometry.py:211-217): the synthetic trajectories' poses, bit for bit."""
+    rel_R = T.rotation.T @ U.rotation
+    axis, angle = axis_angle_from_rotation(rel_R)
+    R = T.rotation @ rotation_from_axis_angle(axis, angle * t)
+    trans = (1.0 - t) * T.translation + t * U.translation
+    return Pose(R, trans)
+
+
 def ray_grid(k):
     """Unit-depth ray directions ((u-cx)/fx, (v-cy)/fy), each (height, width)."""
     u = np.arange(k.width, dtype=np.float64)

@@ -69,6 +69,66 @@ def marching_cubes(store, cfg):
     return TriangleMesh(vertices=v, colors=c, triangles=t[: nt.value])
 
 
+def mesh_blocks(store, cfg):
+    """The per-block layout of marching_cubes(store, cfg): (sorted block
+    keys, vertices per block, triangles per block)."""
+    store._bind(cfg)
+    n = ctypes.c_int64()
+    store._call("rf_mesh_blocks", None, None, None, 0, ctypes.byref(n))
+    k = np.empty(n.value, dtype=np.int64)
+    nv = np.empty(n.value, dtype=np.int64)
+    nt = np.empty(n.value, dtype=np.int64)
+    if n.value:
+        store._call("rf_mesh_blocks", k.ctypes.data_as(L.c_int64_p), nv.ctypes.data_as(L.c_int64_p),
+                    nt.ctypes.data_as(L.c_int64_p), n.value, ctypes.byref(n))
+    return k, nv, nt
+
+
+def merge_shard_meshes(parts):
+    """Interleave the shards' meshes into the unsharded mesh's order (blocks
+    by sorted coordinate, meshing.py:229-231).  ``parts``: per shard
+    (TriangleMesh, keys, vertices per block, triangles per block) -- each
+    shard's own blocks, meshed with its cross-shard neighbours."""
+    rows = []
+    for si, (m, k, nv, nt) in enumerate(parts):
+        vo = np.concatenate([[0], np.cumsum(nv)])
+        to = np.concatenate([[0], np.cumsum(nt)])
+        rows += [(int(k[b]), si, vo[b], vo[b + 1], to[b], to[b + 1]) for b in range(len(k))]
+    rows.sort()
+    vs, cs, ts, base = [], [], [], 0
+    for _, si, v0, v1, t0, t1 in rows:
+        m = parts[si][0]
+        vs.append(m.vertices[v0:v1])
+        cs.append(m.colors[v0:v1])
+        ts.append(m.triangles[t0:t1] - v0 + base)
+        base += v1 - v0
+    if not rows or base == 0:
+        return TriangleMesh()
+    return TriangleMesh(vertices=np.concatenate(vs), colors=np.concatenate(cs),
+                        triangles=np.concatenate(ts).astype(np.int64))
+
+
+def marching_cubes_sharded(stores, cfg):
+    """marching_cubes over a hash-sharded volume (stores connected by
+    volume.connect_shards): every shard meshes its own blocks on its device,
+    reading +x/+y/+z neighbours owned by other shards from their pools, and
+    the parts are merged in block order -- the unsharded mesh, bit for bit."""
+    stores = sorted(stores, key=lambda s: s.shard_rank)
+    G = len(stores)
+    if G < 2 or [s.shard_rank for s in stores] != list(range(G)) or \
+            any(s.shard_count != G for s in stores):
+        raise ValueError("marching_cubes_sharded needs one store per shard rank 0..G-1")
+    for s in stores:
+        s._bind(cfg)
+    vols = (ctypes.c_void_p * G)(*[s._ptr.value for s in stores])
+    for s in stores:  # idempotent (connect_shards does it too)
+        s._call("rf_mesh_connect", vols, G)
+    parts = []
+    for s in stores:
+        parts.append((marching_cubes(s, cfg), *mesh_blocks(s, cfg)))
+    return merge_shard_meshes(parts)
+
+
 def welded_mesh(store, cfg, tol=1e-7):
     """weld(marching_cubes(store, cfg), tol) with both steps on the device
     (rf_marching_cubes_welded): only the welded mesh crosses to the host."""

@@ -373,17 +373,23 @@ class TwoTierStore:
         torch = _torch()
         lib = L.lib()
         if self._own_stream is not None:
-            # a shard with its own stream: ordered after the caller's stream
-            # and before the caller's later work, but never queued behind a
-            # sibling shard's kernels (which may wait in k_shard_sync for it)
+            # A shard with its own stream (shards of one process, one thread
+            # each): the call is ordered after the calling thread's earlier
+            # work, and the thread then stays on the shard's stream, so its
+            # later work is ordered after the call.  The caller's stream is
+            # never made to wait for the shard's: a stream shared by the
+            # shard threads (the default stream) would join every shard's
+            # kernels -- including a k_shard_sync waiting for a sibling whose
+            # next kernels would then queue behind it (a deadlock until the
+            # sync's timeout).
             with torch.cuda.device(self.device):
-                cur = torch.cuda.current_stream()
                 own = self._own_stream
-                own.wait_stream(cur)
+                cur = torch.cuda.current_stream()
+                if cur != own:
+                    own.wait_stream(cur)
+                    torch.cuda.set_stream(own)
                 lib.rf_set_cuda_stream(self._ptr, own.cuda_stream)
-                st = getattr(lib, name)(self._ptr, *args)
-                cur.wait_stream(own)
-                return st
+                return getattr(lib, name)(self._ptr, *args)
         if torch.cuda.current_device() == self.device:  # the common case: no context switch
             lib.rf_set_cuda_stream(self._ptr, torch.cuda.current_stream().cuda_stream)
             return getattr(lib, name)(self._ptr, *args)
@@ -854,6 +860,11 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
     sarr = (ctypes.c_void_p * G)(*[slots[r] for r in range(G)])
     for s in stores:
         s._call("rf_shard_sync_connect", sarr)
+    # marching cubes reads cross-shard neighbour blocks from their owners
+    vols = (ctypes.c_void_p * G)(*[next(s for s in stores if s.shard_rank == r)._ptr.value
+                                   for r in range(G)])
+    for s in stores:
+        s._call("rf_mesh_connect", vols, G)
     group = _ThreadGroup(G, timeout)
     if not route:  # replicated sampling: only the status agreement
         for s in stores:
@@ -897,6 +908,13 @@ def connect_shards_distributed(store, cfg, max_ops=48, cap_keys=None, image=(640
     handles = [None] * G
     dist.all_gather_object(handles, bytes(h), group=group)
     store._call("rf_shard_sync_ipc_open", ctypes.c_char_p(b"".join(handles)))
+    # marching cubes' cross-shard neighbours: the table allocations over IPC
+    h = (ctypes.c_char * 256)()
+    store._call("rf_mesh_ipc_handle", h)
+    handles = [None] * G
+    dist.all_gather_object(handles, (bytes(h), int(cfg.hash_buckets)), group=group)
+    bk = (ctypes.c_int64 * G)(*[b for _, b in handles])
+    store._call("rf_mesh_ipc_open", ctypes.c_char_p(b"".join(x for x, _ in handles)), bk)
     if not route:
         store._router = _ShardRouter(max_ops, lambda: dist.barrier(group=group), agree,
                                      routed=False)

@@ -214,3 +214,39 @@ def test_device_nn_min_d2_matches_oracle(V, n, m):
     assert np.array_equal(out, oracle().nn_min_d2(q, pts))
     with pytest.raises((TypeError, ValueError)):
         K.nn_min_d2(q.astype(np.float32), pts, out)
+
+
+def test_merge_shard_meshes_restores_block_order():
+    """Host merge of the shards' meshes (meshing.merge_shard_meshes): blocks
+    interleave by key, triangle indices are re-based -- the unsharded mesh."""
+    from paper_1709_03763_b200 import meshing as M
+
+    rng = np.random.default_rng(2)
+    keys = np.sort(rng.choice(10_000, size=40, replace=False)).astype(np.int64)
+    nv = rng.integers(0, 9, size=40)
+    nt = np.where(nv >= 3, rng.integers(0, 5, size=40), 0)
+    verts = rng.normal(size=(nv.sum(), 3))
+    cols = rng.uniform(0, 255, size=(nv.sum(), 3))
+    vo = np.concatenate([[0], np.cumsum(nv)])
+    tris = np.concatenate([vo[b] + rng.integers(0, nv[b], size=(nt[b], 3)) for b in range(40)]
+                          + [np.zeros((0, 3), np.int64)]).astype(np.int64)
+    whole = M.TriangleMesh(verts, cols, tris)
+    to = np.concatenate([[0], np.cumsum(nt)])
+    owner = rng.integers(0, 3, size=40)
+    parts = []
+    for s in range(3):
+        bs = np.flatnonzero(owner == s)
+        sv = [verts[vo[b]:vo[b + 1]] for b in bs]
+        sc = [cols[vo[b]:vo[b + 1]] for b in bs]
+        st, base = [], 0
+        for b in bs:
+            st.append(tris[to[b]:to[b + 1]] - vo[b] + base)
+            base += nv[b]
+        m = M.TriangleMesh(np.concatenate(sv + [np.zeros((0, 3))]),
+                           np.concatenate(sc + [np.zeros((0, 3))]),
+                           np.concatenate(st + [np.zeros((0, 3), np.int64)]).astype(np.int64))
+        parts.append((m, keys[bs], nv[bs], nt[bs]))
+    got = M.merge_shard_meshes(parts)
+    assert np.array_equal(got.vertices, whole.vertices)
+    assert np.array_equal(got.colors, whole.colors)
+    assert np.array_equal(got.triangles, whole.triangles)

@@ -6,7 +6,14 @@ protocol the B200 kernels implement:
 * the streaming contract is evaluated over the WHOLE footprint on every
   shard (the first violating key in sorted order is global);
 * a de-integration's failing key is the MIN over shards (one all_reduce
-  per de-integration), and blocks below it are removed + re-added.
+  per de-integration), and blocks below it are removed + re-added -- what
+  k_shard_sync does on the device (every shard's check publishes its first
+  failing key into every shard's verdict slot with a system-scope atomicMin
+  over NVLink, each shard applies the global minimum; k_fuse<kRemoveReadd>
+  removes + re-adds the blocks below it);
+* a correction window whose removal fails re-integrates the entries it
+  already removed (reintegration.py:156-181) on every shard -- the device's
+  rf_correct_windows recovery.
 
 * routed footprints (k_route / rf_route): each rank samples only the pixel
   tiles t with t mod G == rank, keys go to their owners (all-to-all) and
@@ -142,6 +149,31 @@ class ShardModel:
         if fail != big:
             raise self.O.VolumeInconsistencyError("negative weight")
 
+    def correct_entries(self, entries):
+        """reintegration._correct_entries' removal half with its rollback
+        (reintegration.py:156-174), every removal's verdict global."""
+        removed = []
+        try:
+            for kf, old in entries:
+                self.deintegrate(kf, old)
+                removed.append((kf, old))
+        except self.O.VolumeInconsistencyError:
+            for kf, old in removed:
+                self.integrate(kf, old)
+            raise
+
+
+def _ref_correct_entries(O, ref, entries):
+    removed = []
+    try:
+        for kf, old in entries:
+            ref.deintegrate(kf, old)
+            removed.append((kf, old))
+    except O.VolumeInconsistencyError:
+        for kf, old in removed:
+            ref.integrate(kf, old)
+        raise
+
 
 def _worker(rank, world, port, result_path, routed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -163,6 +195,11 @@ def _worker(rank, world, port, result_path, routed=False):
         m.deintegrate(frames[1], wrong)
     except O.VolumeInconsistencyError:
         events.append("inconsistent")
+    m.integrate(frames[0], pose)
+    try:  # entry 1 fails: entry 0's removal is rolled back on every rank
+        m.correct_entries([(frames[0], pose), (frames[1], wrong), (frames[2], pose)])
+    except O.VolumeInconsistencyError:
+        events.append("window")
     far = np.asarray(pose.translation) + np.array([-2.4, 0.0, 0.0])
     moved = S.SPose(S.rot_y(0.5), np.asarray(pose.translation) + np.array([0.3, 0.0, 0.0]))
     m.st.stream(far)
@@ -185,6 +222,11 @@ def _worker(rank, world, port, result_path, routed=False):
             ref.deintegrate(frames[1], wrong)
         except O.VolumeInconsistencyError:
             ref_events.append("inconsistent")
+        ref.integrate(frames[0], pose)
+        try:
+            _ref_correct_entries(O, ref, [(frames[0], pose), (frames[1], wrong), (frames[2], pose)])
+        except O.VolumeInconsistencyError:
+            ref_events.append("window")
         ref.stream(far)
         n_alloc = len(ref.active)
         try:
@@ -202,7 +244,7 @@ def _worker(rank, world, port, result_path, routed=False):
             got = np.concatenate([p[0][i] for p in parts])[order]
             ok = ok and np.array_equal(got, want[i])
         ok = ok and all(p[1] == ref_events for p in parts)
-        ok = ok and ref_events == ["inconsistent", "contract"] and ok_partial
+        ok = ok and ref_events == ["inconsistent", "window", "contract"] and ok_partial
         pk = np.concatenate([p[2][0] for p in parts])
         po = np.argsort(pk)
         ok = ok and np.array_equal(pk[po], want_partial[0])
