@@ -12,8 +12,11 @@ rows = list(csv.reader(open(path)))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+mi = h.index("Metric Name") if "Metric Name" in h else None
 seq = []
 for r in rows[hi + 1:]:
+    if mi is not None and r[mi] != "gpu__time_duration.sum":
+        continue  # launch lists captured with extra metrics
     v = float(r[vi].replace(",", ""))
     unit = r[ui]
     us = v / 1e3 if unit in ("ns", "nsecond") else v * 1e3 if unit in ("ms", "msecond") else v
