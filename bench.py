@@ -419,8 +419,18 @@ def run_b200(args):
     peak_src = "measured" if peak else "fallback"
     peak = peak or 6650.0
     step_ms = total_ms / args.steps
-    alg_bytes = 80.0 * prof.voxels_updated + 40.0 * prof.pixels
-    achieved = alg_bytes / (prof.fuse_ms / 1e3) / 1e9 if prof.fuse_ms > 0 else None
+    # the roofline kernel: the integration (k_fuse<kIntegrate>); removals
+    # (check k_check + removal k_fuse<kApplyRemove>) are reported beside it
+    per_op = prof.integrate_launches > 0
+    if per_op:
+        n_int = int(prof.integrate_launches)
+        alg_bytes = 80.0 * prof.integrate_voxels + 40.0 * prof.integrate_pixels
+        fuse_ms, kernel = prof.integrate_ms, "k_fuse<kIntegrate>"
+    else:  # a library without the per-operation counters
+        n_int = int(prof.fuse_launches)
+        alg_bytes = 80.0 * prof.voxels_updated + 40.0 * prof.pixels
+        fuse_ms, kernel = prof.fuse_ms, "k_fuse<kIntegrate|kApplyRemove>"
+    achieved = alg_bytes / (fuse_ms / 1e3) / 1e9 if fuse_ms > 0 else None
     # DRAM traffic of the same kernel from one ncu --set full capture
     # (tools/prof_workload.py: the bench's keyframes and corrections), with
     # the algorithmic bytes of the SAME captured launches beside it
@@ -429,16 +439,26 @@ def run_b200(args):
     if os.path.exists(tpath):
         tj = json.load(open(tpath))
         traffic, t_alg = tj.get("bytes_per_launch"), tj.get("alg_bytes_per_launch")
+    removal = None
+    if per_op and prof.removal_ops > 0:
+        r_alg = 80.0 * prof.removal_voxels + 40.0 * prof.removal_pixels
+        r_ach = r_alg / (prof.removal_ms / 1e3) / 1e9 if prof.removal_ms > 0 else None
+        removal = {"ops": int(prof.removal_ops),
+                   "kernels": "k_check + k_fuse<kApplyRemove>",
+                   "us_per_op": 1e3 * prof.removal_ms / prof.removal_ops,
+                   "alg_bytes_per_op": r_alg / prof.removal_ops,
+                   "achieved": r_ach, "frac": (r_ach / peak) if r_ach else None}
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "peak_source": peak_src,
             "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
             "traffic": traffic, "traffic_alg_bytes_per_launch": t_alg,
             "traffic_over_alg": (traffic / t_alg) if traffic and t_alg else None,
             "traffic_source": "profiles/fuse_traffic.json (ncu capture of tools/prof_workload.py)",
-            "kernel": "k_fuse<kIntegrate|kApplyRemove>",
-            "launches": int(prof.fuse_launches),
-            "avg_launch_us": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1),
-            "alg_bytes_per_launch": alg_bytes / max(prof.fuse_launches, 1),
+            "kernel": kernel,
+            "launches": n_int,
+            "avg_launch_us": 1e3 * fuse_ms / max(n_int, 1),
+            "alg_bytes_per_launch": alg_bytes / max(n_int, 1),
             "bytes_model": "80 B x voxels_updated + 40 B x H*W per launch",
+            "removal": removal,
             "profiled_steps": prof_steps,
             # device time of each kernel class over the profiled pass's own
             # step time (its steps differ from the timed ones)

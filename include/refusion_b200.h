@@ -139,6 +139,16 @@ typedef struct rf_profile {
     int64_t kernel_launches;     /* every kernel this library launched while profiling */
     int64_t other_launches;      /* streaming, GC and bookkeeping kernels */
     double other_ms;
+    /* per operation: integrations (k_fuse<kIntegrate>) and de-integrations
+     * (the check k_check + the removal k_fuse<kApplyRemove>) */
+    int64_t integrate_launches;
+    double integrate_ms;
+    int64_t integrate_voxels;
+    int64_t integrate_pixels;
+    int64_t removal_ops;
+    double removal_ms;
+    int64_t removal_voxels;
+    int64_t removal_pixels;
 } rf_profile;
 
 /* ---- lifecycle ------------------------------------------------------- */

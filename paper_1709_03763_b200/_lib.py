@@ -116,6 +116,14 @@ class RfProfile(ctypes.Structure):
         ("kernel_launches", ctypes.c_int64),
         ("other_launches", ctypes.c_int64),
         ("other_ms", ctypes.c_double),
+        ("integrate_launches", ctypes.c_int64),
+        ("integrate_ms", ctypes.c_double),
+        ("integrate_voxels", ctypes.c_int64),
+        ("integrate_pixels", ctypes.c_int64),
+        ("removal_ops", ctypes.c_int64),
+        ("removal_ms", ctypes.c_double),
+        ("removal_voxels", ctypes.c_int64),
+        ("removal_pixels", ctypes.c_int64),
     ]
 
 

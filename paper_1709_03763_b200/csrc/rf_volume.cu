@@ -129,6 +129,8 @@ struct rf_volume {
   std::vector<EventPair> events;
   std::vector<cudaEvent_t> event_pool;
   long long prof_voxels = 0, prof_pixels = 0, prof_blocks = 0, prof_launches = 0;
+  long long prof_int_vox = 0, prof_int_pix = 0, prof_rem_vox = 0, prof_rem_pix = 0;
+  long long prof_rem_ops = 0;
   // routed footprints (hash-sharded volume, k_route): this shard's inbox and
   // every shard's (peers opened over IPC are closed on destroy)
   char* route_own = nullptr;
@@ -785,7 +787,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     }
     wait_color(v, kf);  // the check read no colour; the removal does
     {
-      ProfScope ps(v, 0);
+      ProfScope ps(v, 4);
       launch_fuse<kApplyRemove>(v, p);
       launches += 1;
     }
@@ -856,10 +858,21 @@ rf_status batch_end(Batch& b, BatchOutcome& out) {
   if (v->profiling) {
     for (int i = 0; i < b.n_ops; ++i) {
       const int k = b.infos[i].kind;
+      if (k == 2 && out.err_kind && i == out.err_op) v->prof_rem_ops += 1;  // it ran too
       if ((k == 1 || k == 2) && (!out.err_kind || i < out.err_op)) {
         const OpCounters& o = v->h_ops[i];
         v->prof_voxels += static_cast<long long>(o.voxels_updated);
         v->prof_blocks += static_cast<long long>(o.n_touched);
+        const long long npix = static_cast<long long>(b.fparams[i].kf.width) *
+                               b.fparams[i].kf.height;
+        if (k == 1) {
+          v->prof_int_vox += static_cast<long long>(o.voxels_updated);
+          v->prof_int_pix += npix;
+        } else {
+          v->prof_rem_vox += static_cast<long long>(o.voxels_updated);
+          v->prof_rem_pix += npix;
+          v->prof_rem_ops += 1;
+        }
       }
     }
   }
@@ -2098,6 +2111,8 @@ rf_status rf_profile_begin(rf_volume* v) {
   }
   v->events.clear();
   v->prof_voxels = v->prof_pixels = v->prof_blocks = v->prof_launches = 0;
+  v->prof_int_vox = v->prof_int_pix = v->prof_rem_vox = v->prof_rem_pix = 0;
+  v->prof_rem_ops = 0;
   v->profiling = true;
   return RF_OK;
 }
@@ -2110,12 +2125,19 @@ rf_status rf_profile_end(rf_volume* v, rf_profile* out) {
   for (auto& e : v->events) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e.a, e.b);
-    if (e.kind == 0) {
+    if (e.kind == 0 || e.kind == 4) {  // 0 integrate, 4 the removal pass
       p.fuse_launches++;
       p.fuse_ms += ms;
-    } else if (e.kind == 1) {
+      if (e.kind == 0) {
+        p.integrate_launches++;
+        p.integrate_ms += ms;
+      } else {
+        p.removal_ms += ms;
+      }
+    } else if (e.kind == 1) {  // the removal's check (k_check)
       p.check_launches++;
       p.check_ms += ms;
+      p.removal_ms += ms;
     } else if (e.kind == 2) {
       p.footprint_launches++;
       p.footprint_ms += ms;
@@ -2131,6 +2153,11 @@ rf_status rf_profile_end(rf_volume* v, rf_profile* out) {
   p.pixels = v->prof_pixels;
   p.blocks_touched = v->prof_blocks;
   p.kernel_launches = v->prof_launches;
+  p.integrate_voxels = v->prof_int_vox;
+  p.integrate_pixels = v->prof_int_pix;
+  p.removal_ops = v->prof_rem_ops;
+  p.removal_voxels = v->prof_rem_vox;
+  p.removal_pixels = v->prof_rem_pix;
   v->profiling = false;
   *out = p;
   return RF_OK;

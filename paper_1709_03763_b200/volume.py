@@ -839,7 +839,10 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
     device or several; each shard is then driven from its own thread, e.g.
     tests and single-process drivers).  Every integrate / deintegrate /
     allocate_blocks / correct_windows of a shard waits for the other shards'
-    matching call, so the shards must be driven in lockstep."""
+    matching call, so the shards must be driven in lockstep.  Several shards
+    on ONE device wait for each other inside kernels: set
+    CUDA_DEVICE_MAX_CONNECTIONS=32 before CUDA initialises, or two shards'
+    streams may share a hardware queue and stall each other."""
     G = len(stores)
     if G < 2 or any(s.shard_count != G for s in stores) or \
             sorted(s.shard_rank for s in stores) != list(range(G)):

@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# Shards emulated on one GPU wait for each other inside k_shard_sync; with
+# CUDA's default 8 hardware work queues, two shards' streams can share a
+# queue and one shard's waiting kernel then blocks the other's work behind
+# it (a false dependency) until the sync times out.  One queue per stream.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 for p in (REPO, os.path.join(REPO, "tests"), os.path.join(REPO, "oracle")):
     if p not in sys.path:

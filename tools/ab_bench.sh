@@ -8,6 +8,7 @@ for lib in variants/lib_*.so; do
   python -c "
 import json,sys
 d=json.load(open('gpurun_out/ab_$tag.json')); r=d['roofline']
-print('$tag', round(d['value'],1), 'KF/s', round(d['ms_per_step'],2), 'ms/step  fuse', round(r['avg_launch_us'],1), 'us  frac', round(r['frac'],3), ' shares fuse/check/fp', round(r['fuse_ms_share'],3), round(r['check_ms_share'],3), round(r['footprint_ms_share'],3))
+rm=r.get('removal') or {}
+print('$tag', round(d['value'],1), 'KF/s', round(d['ms_per_step'],2), 'ms/step ', r['kernel'], round(r['avg_launch_us'],1), 'us  frac', round(r['frac'],3), ' removal us/op', round(rm.get('us_per_op') or 0,1), ' shares fuse/check/fp', round(r['fuse_ms_share'],3), round(r['check_ms_share'],3), round(r['footprint_ms_share'],3))
 " || tail -3 gpurun_out/ab_$tag.err
 done

@@ -29,6 +29,10 @@ import sys
 import threading
 import time
 
+# one hardware work queue per stream: the shards' streams must not share
+# queues (see tests/conftest.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 

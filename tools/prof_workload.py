@@ -52,7 +52,15 @@ out = {"blocks": store.block_count(), "corrections": a.corrections,
        "blocks_touched": int(prof.blocks_touched),
        "alg_bytes_per_fuse_launch": (80.0 * prof.voxels_updated + 40.0 * prof.pixels)
        / max(prof.fuse_launches, 1),
-       "fuse_us_per_launch_events": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1)}
+       "fuse_us_per_launch_events": 1e3 * prof.fuse_ms / max(prof.fuse_launches, 1),
+       # the roofline kernel (k_fuse<kIntegrate>): the corrections' integrations
+       "integrate_launches": int(prof.integrate_launches),
+       "alg_bytes_per_integrate_launch": (80.0 * prof.integrate_voxels +
+                                          40.0 * prof.integrate_pixels)
+       / max(prof.integrate_launches, 1),
+       "integrate_us_per_launch_events": 1e3 * prof.integrate_ms / max(prof.integrate_launches, 1),
+       "removal_ops": int(prof.removal_ops),
+       "removal_us_per_op_events": 1e3 * prof.removal_ms / max(prof.removal_ops, 1)}
 print(json.dumps(out))
 if a.json:
     json.dump(out, open(a.json, "w"), indent=1)

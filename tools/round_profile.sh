@@ -15,9 +15,12 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 \
   --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/launches_$TAG.csv 2 > gpurun_out/launches_$TAG.json
-timeout 300 python tools/prof_workload.py --build 20 --corrections 1 --json gpurun_out/workload_$TAG.json > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_fuse -s 20 -c 3 \
-  -o gpurun_out/prof_$TAG python tools/prof_workload.py --build 20 --corrections 1 > /dev/null 2>&1
+timeout 300 python tools/prof_workload.py --build 20 --corrections 2 --json gpurun_out/workload_$TAG.json > /dev/null 2>&1
+# the corrections' kernels after the 20 build integrations: the removal
+# (k_check, k_fuse<kApplyRemove>) and the integration (k_fuse<kIntegrate>)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fuse|k_check" -s 20 -c 6 \
+  -o gpurun_out/prof_$TAG python tools/prof_workload.py --build 20 --corrections 2 > /dev/null 2>&1
+python tools/ncu_traffic.py gpurun_out/prof_$TAG.ncu-rep gpurun_out/workload_$TAG.json gpurun_out/fuse_traffic_$TAG.json
 cat gpurun_out/pytest_$TAG.log
 python -c "
 import json; d=json.load(open('gpurun_out/bench_$TAG.json')); r=d['roofline']
