@@ -346,9 +346,13 @@ def run_b200(args):
             picks, nxt = prepare()
             flush.zero_()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # NVTX range "timed" (ncu --nvtx --nvtx-include "timed/" lists
+            # only the timed steps' kernels)
+            torch.cuda.nvtx.range_push("timed")
             a.record(stream)
             corrected += R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
             b.record(stream)
+            torch.cuda.nvtx.range_pop()
             b.synchronize()
             times.append(a.elapsed_time(b))
     # profiled pass (same workload, more events): per-kernel-class device

@@ -441,7 +441,7 @@ void memo_release(rf_volume* v) {
   v->memo_lru.clear();
   v->memo_free.clear();
   if (v->memo_arena) {
-    cudaDeviceSynchronize();  // kernels in flight may still read entries
+    cudaStreamSynchronize(v->stream);  // kernels in flight may still read entries
     cudaFree(v->memo_arena);
   }
   v->memo_arena = nullptr;
@@ -1041,7 +1041,10 @@ rf_status rf_volume_create(const rf_config* cfg, rf_volume** out) {
 rf_status rf_volume_destroy(rf_volume* v) {
   if (!v) return RF_OK;
   cudaSetDevice(v->cfg.device);
-  cudaDeviceSynchronize();
+  // this volume's own work only (other volumes' kernels may be waiting for
+  // their peers inside k_shard_sync)
+  cudaStreamSynchronize(v->stream);
+  if (v->copy_stream) cudaStreamSynchronize(v->copy_stream);
   Table& T = v->T;
   void* ptrs[] = {T.heads, T.keys, T.next, T.nz, T.stamp, T.free_stack, T.returned, T.touched, T.touched_keys, T.tpos,
                   T.new_list, T.pend_tab, T.pend_keys, T.pend_idx, T.spill_keys, T.defer, T.alloc, T.pool, v->d_ws, v->d_u64, v->d_f64, v->d_ops, v->d_wsums, v->d_gc_stamp};

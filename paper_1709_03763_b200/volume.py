@@ -317,6 +317,16 @@ def kf_view_uncached(kf, device=0):
 # the store
 
 
+_GRAVEYARD = []  # dropped connected shards, destroyed at a safe point
+
+
+def release_closed_shards():
+    """Destroy the connected shard stores the garbage collector dropped (call
+    when no shard call is in flight; connect_shards does)."""
+    while _GRAVEYARD:
+        L.lib().rf_volume_destroy(_GRAVEYARD.pop())
+
+
 class TwoTierStore:
     """Device-resident counterpart of volume.TwoTierStore (volume.py:96-123)."""
 
@@ -424,6 +434,15 @@ class TwoTierStore:
 
     def __del__(self):
         try:
+            if self._ptr is not None and self._own_stream is not None:
+                # a connected shard of a one-process group: its destruction
+                # waits for the device, and the garbage collector may run it
+                # in a sibling shard's thread while that sibling's kernels
+                # wait for this thread inside k_shard_sync -- destroy it at
+                # the next safe point instead (release_closed_shards)
+                _GRAVEYARD.append(self._ptr)
+                self._ptr = None
+                return
             self.close()
         except Exception:  # noqa: BLE001 -- interpreter shutdown
             pass
@@ -849,6 +868,7 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
         raise ValueError("connect_shards needs one store per shard rank 0..G-1")
     import torch
 
+    release_closed_shards()  # a safe point: no shard call of this process in flight
     for s in stores:
         s._bind(cfg)
         # each shard runs on its own stream: shards sharing one device must

@@ -20,7 +20,7 @@ print(f"value {d['value']:.1f} KF/s  ms/corr {d['ms_per_step']:.2f}  fuse avg {r
       f"fp {r['footprint_ms_share']:.2f}  e2e {(d.get('e2e') or {}).get('value')}")
 PY
 if [ "${LAUNCHES:-1}" = "1" ]; then
-  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+  timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 \
     --no-cpu-baseline --no-e2e > /dev/null 2>&1
   python tools/launch_summary.py gpurun_out/launches_$TAG.csv 2 > gpurun_out/launches_$TAG.json

@@ -11,7 +11,8 @@ lscpu | grep -E "^CPU\(s\)|Model name" >> gpurun_out/box_$TAG.txt
 timeout 900 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/pytest_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/benchref_$TAG.json 2> gpurun_out/benchref_$TAG.err
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+# the launch list of the timed steps only (NVTX range "timed" in bench.py)
+timeout 1200 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 \
   --no-cpu-baseline --no-e2e > /dev/null 2>&1
 python tools/launch_summary.py gpurun_out/launches_$TAG.csv 2 > gpurun_out/launches_$TAG.json
