@@ -853,7 +853,7 @@ def _route_setup(store, max_ops, cap_keys):
 
 
 def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), timeout=300.0,
-                   route=True):
+                   route=True, verdicts=True):
     """Route the footprints of G shard stores living in ONE process (one
     device or several; each shard is then driven from its own thread, e.g.
     tests and single-process drivers).  Every integrate / deintegrate /
@@ -878,11 +878,14 @@ def connect_shards(stores, cfg, max_ops=48, cap_keys=None, image=(640, 480), tim
             s._own_stream = torch.cuda.Stream()
         s._call("rf_reserve", image[0], image[1], _SYNC_OPS)
     # cross-shard removal verdicts (k_shard_sync): every de-integration fails
-    # on all shards at the same op with the same key, as one volume would
-    slots = {s.shard_rank: _sync_setup(s) for s in stores}
-    sarr = (ctypes.c_void_p * G)(*[slots[r] for r in range(G)])
-    for s in stores:
-        s._call("rf_shard_sync_connect", sarr)
+    # on all shards at the same op with the same key, as one volume would.
+    # (verdicts=False only for drivers that serialise the shards' calls, e.g.
+    # tools/emulated_scaling.py: a shard's call then cannot wait for another's)
+    if verdicts:
+        slots = {s.shard_rank: _sync_setup(s) for s in stores}
+        sarr = (ctypes.c_void_p * G)(*[slots[r] for r in range(G)])
+        for s in stores:
+            s._call("rf_shard_sync_connect", sarr)
     # marching cubes reads cross-shard neighbour blocks from their owners
     vols = (ctypes.c_void_p * G)(*[next(s for s in stores if s.shard_rank == r)._ptr.value
                                    for r in range(G)])

@@ -73,7 +73,10 @@ def main():
         stores = [V.TwoTierStore(block_capacity=cap, shard_rank=r, shard_count=G)
                   for r in range(G)]
         if G > 1 and mode == "routed":
-            V.connect_shards(stores, cfg)
+            # native calls are serialised below, so a shard's call cannot wait
+            # for another's: no device-side removal verdicts (one NVLink round
+            # trip per removal on real GPUs, not in this model)
+            V.connect_shards(stores, cfg, verdicts=False)
         lock = threading.Lock()
         native = [0.0] * G  # per shard: wall time inside its native calls
         for r, s in enumerate(stores):
