@@ -463,12 +463,13 @@ def run_b200(args):
             "alg_bytes_per_launch": alg_bytes / max(n_int, 1),
             "bytes_model": "80 B x voxels_updated + 40 B x H*W per launch",
             "removal": removal,
-            # the whole correction against HBM: algorithmic bytes of every
-            # integration and removal of the profiled steps (80 B / voxel
-            # updated + 40 B / keyframe pixel per op) over those steps' time
-            "step_alg_bytes": (80.0 * prof.voxels_updated + 40.0 * prof.pixels) / prof_steps,
-            "step_frac": ((80.0 * prof.voxels_updated + 40.0 * prof.pixels) / (prof_ms / 1e3)
-                          / 1e9 / peak) if prof_ms else None,
+            # the whole correction against HBM: algorithmic bytes per corrected
+            # keyframe (its removal + integration, profiled steps) x the timed
+            # keyframes/s
+            "step_alg_bytes_per_kf": (80.0 * prof.voxels_updated + 40.0 * prof.pixels)
+            / max(prof_corrected, 1),
+            "step_frac": ((80.0 * prof.voxels_updated + 40.0 * prof.pixels)
+                          / max(prof_corrected, 1) * kf_per_s / 1e9 / peak),
             "profiled_steps": prof_steps,
             # device time of each kernel class over the profiled pass's own
             # step time (its steps differ from the timed ones)

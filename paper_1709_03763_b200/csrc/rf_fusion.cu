@@ -252,63 +252,6 @@ __global__ void k_dw_warp(const double* __restrict__ depth, Intr in, double delt
   target[i] = t;
 }
 
-// exclusive scan of n ints: per-CTA sums, a single-CTA scan of those, apply
-constexpr int kScanBlock = 1024;
-
-__global__ void k_scan_partial(const int* __restrict__ in, int n, int* __restrict__ sums) {
-  __shared__ int s[32];
-  const int i = blockIdx.x * kScanBlock + threadIdx.x;
-  int v = i < n ? in[i] : 0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int k = 0; k < kScanBlock / 32; ++k) t += s[k];
-    sums[blockIdx.x] = t;
-  }
-}
-
-__global__ void k_scan_sums(int* sums, int m) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    int acc = 0;
-    for (int k = 0; k < m; ++k) {
-      const int v = sums[k];
-      sums[k] = acc;
-      acc += v;
-    }
-  }
-}
-
-__global__ void k_scan_apply(const int* __restrict__ in, int n, const int* __restrict__ sums,
-                             int* __restrict__ out) {
-  __shared__ int s[32];
-  const int i = blockIdx.x * kScanBlock + threadIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int v = i < n ? in[i] : 0;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(kFull, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) s[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int w = s[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(kFull, w, o);
-      if (lane >= o) w += y;
-    }
-    s[lane] = w;
-  }
-  __syncthreads();
-  const int before = (warp > 0 ? s[warp - 1] : 0) + x - v;
-  if (i < n) out[i] = sums[blockIdx.x] + before;
-}
-
 __global__ void k_scatter(const int* __restrict__ target, int n, const int* __restrict__ offsets,
                           int* __restrict__ cursor, int* __restrict__ slots) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -970,39 +913,36 @@ rf_status rf_fuse_depth(double* kf_depth, double* kf_weight, const double* frame
                         const double* w_map, int32_t width, int32_t height, double fx, double fy,
                         double cx, double cy, const rf_pose* rel, int32_t blas_order,
                         void* stream) {
-  if (!kf_depth || !kf_weight || !frame_depth || !w_map || !rel || width <= 0 || height <= 0)
+  if (!kf_depth || !kf_weight || !frame_depth || !w_map || !rel || width <= 0 || height <= 0 ||
+      static_cast<long long>(width) * height >= (1LL << 30))
     return RF_INVALID_ARG;
   keep_pool();
   const cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int n = width * height;
-  const int nb = (n + kScanBlock - 1) / kScanBlock;
-  int *target = nullptr, *counts = nullptr, *offsets = nullptr, *cursor = nullptr,
-      *slots = nullptr, *sums = nullptr;
-  double *vwz = nullptr, *vw = nullptr;
-  bool ok = cudaMallocAsync(&target, sizeof(int) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&counts, sizeof(int) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&offsets, sizeof(int) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&cursor, sizeof(int) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&slots, sizeof(int) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&sums, sizeof(int) * (nb + 1), s) == cudaSuccess &&
-            cudaMallocAsync(&vwz, sizeof(double) * n, s) == cudaSuccess &&
-            cudaMallocAsync(&vw, sizeof(double) * n, s) == cudaSuccess;
-  if (ok) {
-    cudaMemsetAsync(counts, 0, sizeof(int) * n, s);
-    cudaMemsetAsync(cursor, 0, sizeof(int) * n, s);
-    const Intr in = make_intr(width, height, fx, fy, cx, cy);
-    k_warp<<<(n + 255) / 256, 256, 0, s>>>(frame_depth, w_map, in, *rel, blas_order, target, vwz,
-                                            vw, counts);
-    k_scan_partial<<<nb, kScanBlock, 0, s>>>(counts, n, sums);
-    k_scan_sums<<<1, 32, 0, s>>>(sums, nb);
-    k_scan_apply<<<nb, kScanBlock, 0, s>>>(counts, n, sums, offsets);
-    k_scatter<<<(n + 255) / 256, 256, 0, s>>>(target, n, offsets, cursor, slots);
-    k_merge<<<(n + 255) / 256, 256, 0, s>>>(kf_depth, kf_weight, n, counts, offsets, slots, vwz, vw);
-  }
-  void* bufs[] = {target, counts, offsets, cursor, slots, sums, vwz, vw};
-  for (void* b : bufs)
-    if (b) cudaFreeAsync(b, s);
-  if (!ok) return RF_CUDA;
+  // one scratch allocation: ints [target | counts | cursor | offsets | slots],
+  // doubles [val_wz | val_w], then the scan's temporary storage
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, static_cast<const int*>(nullptr),
+                                static_cast<int*>(nullptr), n, s);
+  const size_t off_d = (sizeof(int) * 5 * static_cast<size_t>(n) + 255) & ~size_t(255);
+  const size_t off_scan = (off_d + sizeof(double) * 2 * static_cast<size_t>(n) + 255) & ~size_t(255);
+  char* mem = nullptr;
+  if (cudaMallocAsync(&mem, off_scan + scan_bytes, s) != cudaSuccess) return RF_CUDA;
+  int* target = reinterpret_cast<int*>(mem);
+  int* counts = target + n;
+  int* cursor = counts + n;
+  int* offsets = cursor + n;
+  int* slots = offsets + n;
+  double* vwz = reinterpret_cast<double*>(mem + off_d);
+  double* vw = vwz + n;
+  cudaMemsetAsync(counts, 0, sizeof(int) * 2 * n, s);  // counts + cursor
+  const Intr in = make_intr(width, height, fx, fy, cx, cy);
+  k_warp<<<(n + 255) / 256, 256, 0, s>>>(frame_depth, w_map, in, *rel, blas_order, target, vwz, vw,
+                                          counts);
+  cub::DeviceScan::ExclusiveSum(mem + off_scan, scan_bytes, counts, offsets, n, s);
+  k_scatter<<<(n + 255) / 256, 256, 0, s>>>(target, n, offsets, cursor, slots);
+  k_merge<<<(n + 255) / 256, 256, 0, s>>>(kf_depth, kf_weight, n, counts, offsets, slots, vwz, vw);
+  cudaFreeAsync(mem, s);
   return cudaGetLastError() == cudaSuccess ? RF_OK : RF_CUDA;
 }
 

@@ -217,3 +217,41 @@ def test_fuse_color_more_than_64_members_bitexact(KF):
     KF.fuse_color(mkf)
     assert np.array_equal(mkf.color_valid.cpu().numpy(), rkf.color_valid)
     assert np.array_equal(mkf.color.cpu().numpy(), rkf.color)
+
+
+def test_rf_fuse_depth_entry_point_matches_fuse_depth(KF):
+    """The C ABI's standalone rf_fuse_depth (caller-supplied weight map; cub
+    scan + ordered scatter + Eq. 1 merge) gives the keyframe planes the
+    one-call-per-frame path (rf_fuse_frame, behind fuse_depth) gives."""
+    import torch
+
+    from paper_1709_03763_b200 import _lib as L
+    from paper_1709_03763_b200 import geometry as MG
+    from paper_1709_03763_b200.volume import pose_struct
+
+    h, w = 120, 160
+    rng = np.random.default_rng(77)
+    intr = MG.Intrinsics(fx=131.25, fy=131.25, cx=79.5, cy=59.5, width=w, height=h)
+    poses = [MG.Pose(MG.rotation_z(0.004 * i) @ MG.rotation_y(-0.003 * i),
+                     np.array([0.01 * i, -0.005 * i, 0.003 * i])) for i in range(4)]
+    frames = [scene_depth(h, w, intr.fx, intr.cx, intr.cy, rng) for _ in range(4)]
+    kf = None
+    for i, d in enumerate(frames):
+        fo = KF.FrameObservation(i + 1, None, d, poses[i])
+        if kf is None:
+            kf = KF.new_keyframe(fo, intr)
+        KF.fuse_depth(kf, fo)
+    kd = torch.zeros((h, w), dtype=torch.float64, device="cuda:0")
+    kw = torch.zeros_like(kd)
+    for i, d in enumerate(frames):
+        dt = torch.from_numpy(d).cuda()
+        wm = KF.depth_weight_map(dt, intr)  # fuse_depth's map (:245-246)
+        rel = pose_struct(MG.compose(MG.inverse(poses[0]), poses[i]))
+        st = L.lib().rf_fuse_depth(kd.data_ptr(), kw.data_ptr(), dt.data_ptr(),
+                                   wm.contiguous().data_ptr(), w, h, intr.fx, intr.fy, intr.cx,
+                                   intr.cy, L.ctypes.byref(rel), KF.detect_blas_order(),
+                                   torch.cuda.current_stream().cuda_stream)
+        assert st == L.RF_OK
+    torch.cuda.synchronize()
+    assert np.array_equal(kd.cpu().numpy(), kf.depth.cpu().numpy())
+    assert np.array_equal(kw.cpu().numpy(), kf.weight.cpu().numpy())

@@ -40,11 +40,15 @@ for kf, p in zip(kfs, drifted):
 torch.cuda.synchronize()
 lib = L.lib()
 lib.rf_profile_begin(store._ptr)
+# NVTX range "corrections": ncu --nvtx --nvtx-include "corrections/" captures
+# exactly these launches, whose algorithmic bytes --json reports
+torch.cuda.nvtx.range_push("corrections")
 for i in range(a.corrections):
     e = R.LedgerEntry(kfs[i], -1, drifted[i], gt_kf[i], 0, gt_kf[i])
     V.correct_entries(store, [e], cfg, next_center=gt_kf[i].translation)
     drifted[i] = gt_kf[i]
 torch.cuda.synchronize()
+torch.cuda.nvtx.range_pop()
 prof = L.RfProfile()
 lib.rf_profile_end(store._ptr, L.ctypes.byref(prof))
 out = {"blocks": store.block_count(), "corrections": a.corrections,

@@ -19,7 +19,7 @@ python tools/launch_summary.py gpurun_out/launches_$TAG.csv 2 > gpurun_out/launc
 timeout 300 python tools/prof_workload.py --build 20 --corrections 2 --json gpurun_out/workload_$TAG.json > /dev/null 2>&1
 # the corrections' kernels after the 20 build integrations: the removal
 # (k_check, k_fuse<kApplyRemove>) and the integration (k_fuse<kIntegrate>)
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_fuse|k_check" -s 20 -c 6 \
+timeout 900 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "corrections/" -k regex:"k_fuse|k_check" \
   -o gpurun_out/prof_$TAG python tools/prof_workload.py --build 20 --corrections 2 > /dev/null 2>&1
 python tools/ncu_traffic.py gpurun_out/prof_$TAG.ncu-rep gpurun_out/workload_$TAG.json gpurun_out/fuse_traffic_$TAG.json
 cat gpurun_out/pytest_$TAG.log
