@@ -31,7 +31,6 @@
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 
 struct Intr {
   int w, h;
