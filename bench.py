@@ -393,15 +393,16 @@ def run_b200(args):
         h2d = 0
         etimes = []
         e_corr = 0
-        for _ in range(args.steps):
-            picks, nxt = prepare()
-            flush.zero_()
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            e_corr += R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
-            torch.cuda.synchronize()
-            etimes.append(time.perf_counter() - t1)
-            h2d += len(picks) * H * W * (8 + 8 + 24)
+        with ClockSampler(local) as eclk:
+            for _ in range(args.steps):
+                picks, nxt = prepare()
+                flush.zero_()
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                e_corr += R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+                torch.cuda.synchronize()
+                etimes.append(time.perf_counter() - t1)
+                h2d += len(picks) * H * W * (8 + 8 + 24)
         e_total = sum(etimes)
         if world > 1:
             t = torch.tensor([e_total], dtype=torch.float64, device=dev)
@@ -412,6 +413,9 @@ def run_b200(args):
                "h2d_bytes_per_step": h2d // args.steps,
                # per pick: the window result read back (rf_window_result + op records)
                "d2h_bytes_per_step": args.m * (64 + 8 * 88),
+               "clocks": eclk.summary(),
+               "note": "the corrections after the timed and profiled ones (the pose-update "
+                       "stream continues), so per-step work differs from the timed steps'",
                "path": "reintegration.correct_topk on keyframes held in pinned host memory: "
                        "every correction uploads the picked keyframes' planes (40 B/px) and "
                        "reads the window result back; host wall clock"}
