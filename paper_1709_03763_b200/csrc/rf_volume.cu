@@ -745,16 +745,10 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
       }
     }
     // cached key list or full ray sampling (decided on the device), then
-    // the allocation of the missing blocks -- by the footprint kernel's last
-    // CTA when the footprint is memoised (usually nothing to create), else by
-    // k_commit over the whole grid
-    fp.commit_in_tail = (memo && existed && !v->route_on) ? 1 : 0;
+    // the allocation of the missing blocks
     launch(k_footprint<false>, footprint_grid(v, kf), 256, 0, v->stream, v->T, fp);
-    launches += 1;
-    if (!fp.commit_in_tail) {
-      launch(k_commit, v->n_sms * 2, 256, 0, v->stream, v->T, fp);
-      launches += 1;
-    }
+    launch(k_commit, v->n_sms * 2, 256, 0, v->stream, v->T, fp);
+    launches += 2;
   }
   FuseParams p = fuse_params(v, kf, pose, op);
   p.capture = memo;
