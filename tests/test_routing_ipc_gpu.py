@@ -3,7 +3,9 @@ connect_shards_distributed): two ranks on the one device of this run, a
 gloo process group for the barrier and the status agreement, CUDA IPC for the
 inboxes -- the multi-GPU code path with both shards on one GPU.  The union of
 the ranks' volumes must equal a single volume bit for bit, and an error on
-the shards must surface on both ranks."""
+the shards must surface on both ranks.  Each rank's marching cubes reads its
+cross-shard neighbours from the other process's pool (rf_mesh_ipc_open): the
+ranks' meshes merged in block order equal the single volume's mesh."""
 
 import os
 import socket
@@ -60,6 +62,12 @@ def _worker(rank, world, port, out_dir):
     frames, old, new = _scene()
     _run(V, S, store, cfg, frames, old, new)
     keys, d, w, c = store.export()
+    from paper_1709_03763_b200 import meshing as M
+
+    dist.barrier()  # both volumes final before either meshes (peer reads)
+    mesh = M.marching_cubes(store, cfg)
+    mk, mnv, mnt = M.mesh_blocks(store, cfg)
+    dist.barrier()  # the peer's pool stays alive until both have meshed
     # a contract error raised on every rank
     err = "none"
     try:
@@ -67,7 +75,8 @@ def _worker(rank, world, port, out_dir):
         V.integrate(store, frames[0], old[0], cfg)
     except StreamingContractError:
         err = "contract"
-    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), keys=keys, d=d, w=w, c=c, err=err)
+    np.savez(os.path.join(out_dir, f"rank{rank}.npz"), keys=keys, d=d, w=w, c=c, err=err,
+             mv=mesh.vertices, mc=mesh.colors, mt=mesh.triangles, mk=mk, mnv=mnv, mnt=mnt)
     dist.barrier()
     store.close()
     dist.destroy_process_group()
@@ -93,3 +102,12 @@ def test_two_process_ipc_routed_equals_single(tmp_path):
     for i, name in ((1, "d"), (2, "w"), (3, "c")):
         assert np.array_equal(np.concatenate([p[name] for p in parts])[order], want[i])
     assert all(str(p["err"]) == "contract" for p in parts)
+    from paper_1709_03763_b200 import meshing as M
+
+    got = M.merge_shard_meshes([(M.TriangleMesh(p["mv"], p["mc"], p["mt"]), p["mk"], p["mnv"],
+                                 p["mnt"]) for p in parts])
+    ref = M.marching_cubes(single, cfg)
+    assert ref.n_triangles > 100
+    assert np.array_equal(got.vertices, ref.vertices)
+    assert np.array_equal(got.colors, ref.colors)
+    assert np.array_equal(got.triangles, ref.triangles)
