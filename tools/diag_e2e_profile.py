@@ -1,7 +1,8 @@
 """Where the end-to-end correction time goes: the bench's corrections with
-keyframes resident vs uploaded from pinned host memory, each with the wall
-time, the device-event time around the call, and rf_profile's per-kernel-class
-device time (fuse / check / footprint / other).  Diagnostic only."""
+keyframes resident vs uploaded from pinned host memory -- each run on a fresh
+volume with the same event sequence, so both apply exactly the same
+corrections -- with the wall time, the device-event time around the call, and
+(profiled runs) rf_profile's per-kernel-class device time.  Diagnostic only."""
 
 import ctypes
 import json
@@ -30,60 +31,71 @@ def main():
     kfs = B.build_keyframes(n_kf, gt_f, dr)
     cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
                          hash_buckets=1 << 21)
-    store = V.TwoTierStore(block_capacity=2_000_000)
-    for kf, p in zip(kfs, dr):
-        V.stream(store, p.translation, cfg)
-        V.integrate(store, kf, p, cfg)
-    torch.cuda.synchronize()
     n_anchors = (n_kf + B.EVENT_EVERY_KF - 1) // B.EVENT_EVERY_KF
     events = B.make_events(n_anchors, 4 * steps + 8)
-    scen = B.Scenario(R, G, SY, gt, dr, kfs, events)
     lib = L.lib()
     stream = torch.cuda.current_stream()
-    idx = [0]
+    host = {id(kf): kf.to_host(pinned=True) for kf in kfs}
 
-    def one():
-        ev = scen.event(idx[0])
-        idx[0] += 1
-        R.apply_pose_update(scen.ledger, ev)
-        picks = R.select_topk(scen.ledger, B.M_TOPK)
-        nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation
+    def run(label, on_host, profile):
+        """A fresh volume and ledger, the same event sequence: every run applies
+        exactly the same corrections, so runs differ only in the keyframes'
+        location (HBM or pinned host memory) and in profiling."""
+        store = V.TwoTierStore(block_capacity=2_000_000)
+        for kf, p in zip(kfs, dr):
+            V.stream(store, p.translation, cfg)
+            V.integrate(store, kf, p, cfg)
+        scen = B.Scenario(R, G, SY, gt, dr, kfs, events)
+        if on_host:
+            for e in scen.ledger.entries:
+                e.kf = host[id(e.kf)]
         torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        t = time.perf_counter()
-        a.record(stream)
-        R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
-        b.record(stream)
-        b.synchronize()
-        return 1e3 * (time.perf_counter() - t), a.elapsed_time(b)
+        idx = [0]
 
-    def phase(label):
+        def one():
+            ev = scen.event(idx[0])
+            idx[0] += 1
+            R.apply_pose_update(scen.ledger, ev)
+            picks = R.select_topk(scen.ledger, B.M_TOPK)
+            nxt = scen.ledger.entries[picks[0] - 1].target_pose.translation
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            t = time.perf_counter()
+            a.record(stream)
+            R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
+            b.record(stream)
+            b.synchronize()
+            return 1e3 * (time.perf_counter() - t), a.elapsed_time(b)
+
         for _ in range(3):
             one()
-        lib.rf_profile_begin(store._ptr)
+        if profile:
+            lib.rf_profile_begin(store._ptr)
         walls, devs = [], []
         for _ in range(steps):
             w, d = one()
             walls.append(w)
             devs.append(d)
-        prof = L.RfProfile()
-        lib.rf_profile_end(store._ptr, ctypes.byref(prof))
-        print(json.dumps({"mode": label, "wall_ms": round(sum(walls) / steps, 3),
-                          "event_ms": round(sum(devs) / steps, 3),
-                          "fuse_ms": round(prof.fuse_ms / steps, 3),
-                          "check_ms": round(prof.check_ms / steps, 3),
-                          "footprint_ms": round(prof.footprint_ms / steps, 3),
-                          "other_ms": round(prof.other_ms / steps, 3)}), flush=True)
+        out = {"mode": label, "profiled": profile, "wall_ms": round(sum(walls) / steps, 3),
+               "event_ms": round(sum(devs) / steps, 3)}
+        if profile:
+            prof = L.RfProfile()
+            lib.rf_profile_end(store._ptr, ctypes.byref(prof))
+            out.update({"integrate_ms": round(prof.integrate_ms / steps, 3),
+                        "removal_ms": round(prof.removal_ms / steps, 3),
+                        "fuse_ms": round(prof.fuse_ms / steps, 3),
+                        "check_ms": round(prof.check_ms / steps, 3),
+                        "footprint_ms": round(prof.footprint_ms / steps, 3),
+                        "other_ms": round(prof.other_ms / steps, 3)})
+        print(json.dumps(out), flush=True)
+        store.close()
+        torch.cuda.synchronize()
 
-    phase("resident")
-    host = {id(kf): kf.to_host(pinned=True) for kf in kfs}
-    for e in scen.ledger.entries:
-        e.kf = host[id(e.kf)]
-    phase("host")
-    for e in scen.ledger.entries:
-        e.kf = kfs[e.kf_id - 1]
-    phase("resident")
+    for profile in (False, True):
+        run("resident", False, profile)
+        run("host", True, profile)
+    run("resident", False, False)
 
 
 if __name__ == "__main__":
