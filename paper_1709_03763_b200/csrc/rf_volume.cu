@@ -107,9 +107,15 @@ struct rf_volume {
     cudaEvent_t color_ready = nullptr;  // colour plane uploaded (after depth + weight)
     const void* host = nullptr;  // host depth pointer staged in this batch
     bool used = false;
+    unsigned gen = 0;  // refills of this slot (its upload flags' value)
   };
   std::vector<StageSlot> stage;
   std::unordered_map<const double*, cudaEvent_t> color_ready;  // staged colour plane -> upload event
+  // upload flags: per slot {depth + weight, colour}, written by the copy stream
+  // after the planes (the kernels wait on them instead of the stream on events)
+  unsigned* d_stage_flags = nullptr;
+  size_t stage_flags_cap = 0;  // slots
+  std::unordered_map<const double*, std::pair<const unsigned*, unsigned>> upload_flag;
   cudaStream_t copy_stream = nullptr;
   int stage_next = 0;
   int fp_grid_cap = 148 * 8;
@@ -626,6 +632,7 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
                       std::vector<int>& slot_of) {
   out.assign(in, in + n);
   slot_of.assign(n, -1);
+  v->upload_flag.clear();  // flags are looked up only for this call's staged views
   bool any = false;
   for (int i = 0; i < n; ++i) any |= in[i].planes_on_host != 0;
   if (!any) return RF_OK;
@@ -634,6 +641,15 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
   // every entry of one call (window) must be resident at once
   const size_t ring = std::max<size_t>(kStageSlots, static_cast<size_t>(n));
   if (v->stage.size() < ring) v->stage.resize(ring);
+  if (v->stage_flags_cap < v->stage.size()) {  // (all earlier work is complete here)
+    RF_CUDA_TRY(v, cudaStreamSynchronize(v->copy_stream));
+    if (v->d_stage_flags) cudaFree(v->d_stage_flags);
+    v->d_stage_flags = nullptr;
+    RF_CUDA_TRY(v, cudaMalloc(&v->d_stage_flags, sizeof(unsigned) * 2 * v->stage.size()));
+    RF_CUDA_TRY(v, cudaMemset(v->d_stage_flags, 0, sizeof(unsigned) * 2 * v->stage.size()));
+    v->stage_flags_cap = v->stage.size();
+    for (auto& sl : v->stage) sl.gen = 0;
+  }
   for (auto& sl : v->stage) sl.host = nullptr;
   for (int i = 0; i < n; ++i) {
     const rf_kf_view& k = in[i];
@@ -662,11 +678,18 @@ rf_status stage_views(rf_volume* v, const rf_kf_view* in, int n, std::vector<rf_
       cudaMemcpyAsync(sl.buf + npix, k.weight, sizeof(double) * npix, cudaMemcpyHostToDevice,
                       v->copy_stream);
       RF_CUDA_TRY(v, cudaEventRecord(sl.ready, v->copy_stream));
+      sl.gen = sl.gen % 255 + 1;  // a byte value, never 0 (the flags' initial value)
+      const unsigned val = sl.gen * 0x01010101u;
+      unsigned* flag = v->d_stage_flags + 2 * s;
+      cudaMemsetAsync(flag, static_cast<int>(sl.gen), sizeof(unsigned), v->copy_stream);
+      v->upload_flag[sl.buf] = {flag, val};
       if (k.color) {
         cudaMemcpyAsync(sl.buf + 2 * npix, k.color, sizeof(double) * 3 * npix,
                         cudaMemcpyHostToDevice, v->copy_stream);
         RF_CUDA_TRY(v, cudaEventRecord(sl.color_ready, v->copy_stream));
         v->color_ready[sl.buf + 2 * npix] = sl.color_ready;
+        cudaMemsetAsync(flag + 1, static_cast<int>(sl.gen), sizeof(unsigned), v->copy_stream);
+        v->upload_flag[sl.buf + 2 * npix] = {flag + 1, val};
       }
       sl.used = true;
       sl.host = k.depth;
@@ -693,6 +716,14 @@ void stage_consumed(rf_volume* v, const std::vector<int>& slot_of, int i) {
     cudaEventRecord(v->stage[slot_of[i]].consumed, v->stream);
 }
 
+// The upload flag of a staged plane, {nullptr, 0} for a caller-resident one.
+std::pair<const unsigned*, unsigned> upload_flag_of(const rf_volume* v, const double* plane) {
+  if (!plane || v->upload_flag.empty()) return {nullptr, 0u};
+  auto it = v->upload_flag.find(plane);
+  return it == v->upload_flag.end() ? std::pair<const unsigned*, unsigned>{nullptr, 0u}
+                                    : it->second;
+}
+
 // A staged keyframe's colour plane may still be uploading: the kernels that
 // read colour (integrate / removal apply) wait for it.
 void wait_color(rf_volume* v, const rf_kf_view* kf) {
@@ -704,10 +735,17 @@ void wait_color(rf_volume* v, const rf_kf_view* kf) {
 // mode: 0 integrate, 1 deintegrate, 2 allocate only.
 void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
-  if (kf->ready_event) cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
+  // staged planes: the op's first kernel waits on the upload flag on the
+  // device; other events (a caller's own uploads) on the stream
+  const auto up = upload_flag_of(v, kf->depth);
+  const auto upc = upload_flag_of(v, kf->color);
+  if (kf->ready_event && !up.first)
+    cudaStreamWaitEvent(v->stream, static_cast<cudaEvent_t>(kf->ready_event), 0);
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
+  fp.wait_flag = up.first;
+  fp.wait_val = up.second;
   bool existed = false;
   FpEntry* memo = nullptr;
   if (v->route_on) {  // the footprint arrives in this shard's inbox (k_route)
@@ -738,7 +776,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
       if (existed) {  // the guard must be known before the cached keys are used
         const long long npix = static_cast<long long>(kf->width) * kf->height;
         launch(k_kf_hash, v->n_sms * 4, 256, 0, v->stream, kf->depth, kf->weight, npix,
-               &v->d_ops[op].kf_hash);
+               &v->d_ops[op].kf_hash, up.first, up.second);
         launches += 1;
       } else {  // a new entry samples the rays anyway: hash the planes there
         fp.hash_inline = 1;
@@ -761,10 +799,16 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
     if (v->profiling) v->prof_launches += launches + 1;
     return;
   }
-  if (mode == 0) wait_color(v, kf);
   if (mode == 0) {
+    if (upc.first) {  // the colour upload: waited for by the kernel
+      p.wait_flag = upc.first;
+      p.wait_val = upc.second;
+    } else {
+      wait_color(v, kf);
+    }
     ProfScope ps(v, 0);
     launch_fuse<kIntegrate>(v, p);
+    p.wait_flag = nullptr;
     launches += 1;
   } else {
     {
@@ -785,7 +829,13 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
              60ull * 2000000000ull);  // ~60 s at 2 GHz: a peer that never comes is an error
       launches += 1;
     }
-    wait_color(v, kf);  // the check read no colour; the removal does
+    // the check read no colour; the removal does
+    if (upc.first) {
+      p.wait_flag = upc.first;
+      p.wait_val = upc.second;
+    } else {
+      wait_color(v, kf);
+    }
     {
       ProfScope ps(v, 4);
       launch_fuse<kApplyRemove>(v, p);
@@ -1066,6 +1116,7 @@ rf_status rf_volume_destroy(rf_volume* v) {
     if (sl.consumed) cudaEventDestroy(sl.consumed);
   }
   if (v->copy_stream) cudaStreamDestroy(v->copy_stream);
+  if (v->d_stage_flags) cudaFree(v->d_stage_flags);
   for (int s = 0; s < kMaxShards; ++s) {
     if (v->route_ipc[s]) cudaIpcCloseMemHandle(v->route_peer[s]);
     if (v->sync_ipc[s]) cudaIpcCloseMemHandle(v->sync_peer[s]);
