@@ -383,9 +383,26 @@ def run_b200(args):
     # ---- e2e: same steps through the public API with HOST keyframes ------
     e2e = None
     if not args.no_e2e:
-        host = {id(kf): kf.to_host(pinned=True) for kf in keyframes}
-        for e in scen.ledger.entries:
-            e.kf = host[id(e.kf)]
+        # the SAME corrections as the timed pass: rebuild the volume (untimed,
+        # resident keyframes, bit-identical to the first build), restart the
+        # pose-update stream, and replay warm-up + timed steps with every
+        # ledger entry's keyframe in pinned host memory
+        store.close()
+        del store
+        store = V.TwoTierStore(block_capacity=cap, shard_rank=rank, shard_count=world)
+        if world > 1:
+            V.connect_shards_distributed(store, cfg, route=routed)
+        for kf, pose in zip(keyframes, drifted):
+            V.stream(store, pose.translation, cfg)
+            V.integrate(store, kf, pose, cfg)
+        torch.cuda.synchronize()
+        if store.block_count() != n_blocks:
+            raise RuntimeError("e2e rebuild differs from the first build")
+        host = [kf.to_host(pinned=True) for kf in keyframes]
+        scen = Scenario(R, G, SY, gt_kf, drifted, host, scen.events)
+        step_idx[0] = 0
+        if world > 1:
+            dist.barrier()
         for _ in range(args.warmup):  # first uploads size the allocator's pools
             picks, nxt = prepare()
             R.correct_topk(store, scen.ledger, picks, cfg, next_center=nxt)
@@ -414,8 +431,8 @@ def run_b200(args):
                # per pick: the window result read back (rf_window_result + op records)
                "d2h_bytes_per_step": args.m * (64 + 8 * 88),
                "clocks": eclk.summary(),
-               "note": "the corrections after the timed and profiled ones (the pose-update "
-                       "stream continues), so per-step work differs from the timed steps'",
+               "note": "the timed pass's corrections replayed (volume rebuilt untimed, "
+                       "pose-update stream restarted): same per-step work as `value`",
                "path": "reintegration.correct_topk on keyframes held in pinned host memory: "
                        "every correction uploads the picked keyframes' planes (40 B/px) and "
                        "reads the window result back; host wall clock"}
