@@ -13,7 +13,11 @@ the finalize: keyframes re-integrated per second on this shard.  Device timed
 with CUDA events; the building frames come from the device port of the
 reference renderer (bit-identical to synth.py).
 
-    python tools/bench_c3_slice.py [--keyframes 2000] [--kappa 10] [--shards 8]"""
+    python tools/bench_c3_slice.py [--keyframes 2000] [--kappa 10] [--shards 8]
+
+C5's single-GPU slice (BASELINE configs[4]: 4,000 keyframes at 4 mm, the
+scaling sweep's volume) is the same run at --keyframes 4000 --kappa 5
+--voxel 0.004 --tag C5 (the building stands in for C5's scene; shard 0 of 8)."""
 
 import argparse
 import json
@@ -78,6 +82,9 @@ def main():
     ap.add_argument("--shards", type=int, default=8)
     ap.add_argument("--rank", type=int, default=0)
     ap.add_argument("--blocks", type=int, default=2_400_000)
+    ap.add_argument("--voxel", type=float, default=None, help="voxel size (default: the bench's 5 mm)")
+    ap.add_argument("--hash-bits", type=int, default=21)
+    ap.add_argument("--tag", default="C3")
     args = ap.parse_args()
 
     import numpy as np
@@ -106,8 +113,9 @@ def main():
     torch.cuda.synchronize()
     fuse_s = time.time() - t0
 
-    cfg = V.VolumeConfig(voxel_size=B.VOXEL, mu=B.MU, stream_radius=B.RADIUS,
-                         hash_buckets=1 << 21)
+    voxel = args.voxel or B.VOXEL
+    cfg = V.VolumeConfig(voxel_size=voxel, mu=B.MU, stream_radius=B.RADIUS,
+                         hash_buckets=1 << args.hash_bits)
     store = V.TwoTierStore(block_capacity=args.blocks, shard_rank=args.rank,
                            shard_count=args.shards)
     store._bind(cfg)
@@ -139,12 +147,13 @@ def main():
     b_ev.synchronize()
     fin_ms = a_ev.elapsed_time(b_ev)
     out = {
-        "config": f"C3 single-GPU slice: building 40x40x3 m (outer RoomShell + interior "
+        "config": f"{args.tag} single-GPU slice: building 40x40x3 m (outer RoomShell + interior "
                   f"BoxSolid walls with door gaps, 3x3 rooms), {n_kf * kappa} frames -> "
-                  f"{n_kf} keyframes (kappa {kappa}), 5 mm, drifted poses, loop closure "
+                  f"{n_kf} keyframes (kappa {kappa}), {voxel * 1e3:g} mm, drifted poses, loop closure "
                   f"(every anchor to its true pose) -> finalize; shard {args.rank} of "
                   f"{args.shards} (replicated sampling, owned blocks), all keyframes in HBM",
         "frames": n_kf * kappa, "keyframes": n_kf, "fusion_s": round(fuse_s, 1),
+        "device_mem_used_gb": round((lambda f: (f[1] - f[0]) / 1e9)(torch.cuda.mem_get_info()), 1),
         "build_integrate_s": round(build_s, 2), "shard_blocks": blocks,
         "finalize": {"keyframes_corrected": n, "ms": fin_ms,
                      "keyframes_per_s": n / (fin_ms / 1e3), "wall_s": round(time.time() - t0, 2),
