@@ -276,6 +276,7 @@ struct Batch {
   std::vector<OpInfo> infos;
   std::vector<FuseParams> fparams;  // per op (fuse ops only)
   int gc_op = -1;
+  int gc_pending = -1;  // a GC op whose launch waits to be merged with the next stream op
   // routed volume: next inbox op to consume (route_force >= 0 overrides)
   int route_next = 0;
   int route_force = -1;
@@ -316,8 +317,12 @@ int next_op(Batch& b) {
   return b.n_ops++;
 }
 
+void flush_gc(Batch& b);
+
 void op_stream(Batch& b, const double c[3]) {
   rf_volume* v = b.v;
+  const int gc = b.gc_pending;  // merged into this op's pass when it launches one
+  b.gc_pending = -1;
   const int op = next_op(b);
   b.infos.push_back({0, -1});
   b.fparams.emplace_back();
@@ -334,8 +339,15 @@ void op_stream(Batch& b, const double c[3]) {
   const bool same = b.has_center && c[0] == b.center[0] && c[1] == b.center[1] && c[2] == b.center[2];
   if (!same) {
     ProfScope ps(v, 3);
-    launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, p);
+    if (gc >= 0)
+      launch(k_gc_stream, v->n_sms * 4, 256, 0, v->stream, v->T, gc, &v->d_ops[gc].n_new,
+             v->d_gc_stamp, v->gc_epoch, p);
+    else
+      launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, p);
     if (v->profiling) v->prof_launches += 1;
+  } else if (gc >= 0) {
+    b.gc_pending = gc;
+    flush_gc(b);
   }
   // relocation (volume.py:358-364): centre moved more than one block span
   int reloc = 0;
@@ -735,6 +747,7 @@ void wait_color(rf_volume* v, const rf_kf_view* kf) {
 // mode: 0 integrate, 1 deintegrate, 2 allocate only.
 void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
+  flush_gc(b);
   // staged planes: the op's first kernel waits on the upload flag on the
   // device; other events (a caller's own uploads) on the stream
   const auto up = upload_flag_of(v, kf->depth);
@@ -845,8 +858,23 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   if (v->profiling) v->prof_launches += launches;
 }
 
+// A GC op is launched lazily: merged with the stream op that follows it
+// (k_gc_stream), or on its own before any other launch (flush_gc).
+void flush_gc(Batch& b) {
+  if (b.gc_pending < 0) return;
+  rf_volume* v = b.v;
+  const int op = b.gc_pending;
+  b.gc_pending = -1;
+  // freed count lands in the op's n_new field
+  ProfScope ps(v, 3);
+  launch(k_gc, v->n_sms * 8, 256, 0, v->stream, v->T, op, v->d_ws, &v->d_ops[op].n_new,
+         v->d_gc_stamp, v->gc_epoch);
+  if (v->profiling) v->prof_launches += 1;
+}
+
 void op_gc(Batch& b) {
   rf_volume* v = b.v;
+  flush_gc(b);
   const int op = next_op(b);
   b.infos.push_back({3, -1});
   b.fparams.emplace_back();
@@ -855,11 +883,7 @@ void op_gc(Batch& b) {
     cudaMemsetAsync(v->d_gc_stamp, 0, sizeof(unsigned) * v->cfg.hash_buckets, v->stream);
     v->gc_epoch = 1;
   }
-  // freed count lands in the op's n_new field
-  ProfScope ps(v, 3);
-  launch(k_gc, v->n_sms * 8, 256, 0, v->stream, v->T, op, v->d_ws, &v->d_ops[op].n_new,
-         v->d_gc_stamp, v->gc_epoch);
-  if (v->profiling) v->prof_launches += 1;
+  b.gc_pending = op;
 }
 
 // A connected shard's call that may de-integrate: a new sync generation;
@@ -884,6 +908,7 @@ struct BatchOutcome {
 // the ops that executed.
 rf_status batch_end(Batch& b, BatchOutcome& out) {
   rf_volume* v = b.v;
+  flush_gc(b);
   const int n = std::max(b.n_ops, 1);
   cudaMemcpyAsync(v->h_ops, v->d_ops, sizeof(OpCounters) * n, cudaMemcpyDeviceToHost, v->stream);
   cudaMemcpyAsync(v->h_ws, v->d_ws, sizeof(WinState), cudaMemcpyDeviceToHost, v->stream);
