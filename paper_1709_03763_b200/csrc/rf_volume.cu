@@ -277,6 +277,8 @@ struct Batch {
   std::vector<FuseParams> fparams;  // per op (fuse ops only)
   int gc_op = -1;
   int gc_pending = -1;  // a GC op whose launch waits to be merged with the next stream op
+  bool st_pending = false;  // a stream op whose scan waits to be merged into the next footprint
+  StreamParams st_p{};
   // routed volume: next inbox op to consume (route_force >= 0 overrides)
   int route_next = 0;
   int route_force = -1;
@@ -319,6 +321,17 @@ int next_op(Batch& b) {
 
 void flush_gc(Batch& b);
 
+// A pending stream op runs on its own (k_stream) unless a footprint launch
+// took it (op_fuse).
+void flush_stream(Batch& b) {
+  if (!b.st_pending) return;
+  b.st_pending = false;
+  rf_volume* v = b.v;
+  ProfScope ps(v, 3);
+  launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, b.st_p);
+  if (v->profiling) v->prof_launches += 1;
+}
+
 void op_stream(Batch& b, const double c[3]) {
   rf_volume* v = b.v;
   const int gc = b.gc_pending;  // merged into this op's pass when it launches one
@@ -337,14 +350,19 @@ void op_stream(Batch& b, const double c[3]) {
   p.ws = v->d_ws;
   // tiers are a function of the centre: an unchanged centre moves nothing
   const bool same = b.has_center && c[0] == b.center[0] && c[1] == b.center[1] && c[2] == b.center[2];
+  // (a pending stream op of an unchanged centre stays mergeable: nothing
+  // between them changes the blocks)
   if (!same) {
-    ProfScope ps(v, 3);
-    if (gc >= 0)
+    flush_stream(b);
+    if (gc >= 0) {
+      ProfScope ps(v, 3);
       launch(k_gc_stream, v->n_sms * 4, 256, 0, v->stream, v->T, gc, &v->d_ops[gc].n_new,
              v->d_gc_stamp, v->gc_epoch, p);
-    else
-      launch(k_stream, v->n_sms * 4, 256, 0, v->stream, v->T, p);
-    if (v->profiling) v->prof_launches += 1;
+      if (v->profiling) v->prof_launches += 1;
+    } else {  // merged into the next footprint launch, or flushed
+      b.st_pending = true;
+      b.st_p = p;
+    }
   } else if (gc >= 0) {
     b.gc_pending = gc;
     flush_gc(b);
@@ -748,6 +766,15 @@ void wait_color(rf_volume* v, const rf_kf_view* kf) {
 void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int entry) {
   rf_volume* v = b.v;
   flush_gc(b);
+  // a pending stream op's scan rides on this op's footprint launch
+  FpStream merged{};
+  if (b.st_pending) {
+    std::memcpy(merged.old_c, b.st_p.old_c, sizeof(merged.old_c));
+    std::memcpy(merged.new_c, b.st_p.new_c, sizeof(merged.new_c));
+    merged.has_old = b.st_p.has_old;
+    merged.op = b.st_p.op;
+    b.st_pending = false;
+  }
   // staged planes: the op's first kernel waits on the upload flag on the
   // device; other events (a caller's own uploads) on the stream
   const auto up = upload_flag_of(v, kf->depth);
@@ -757,6 +784,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
   const int op = next_op(b);
   b.infos.push_back({mode == 0 ? 1 : (mode == 1 ? 2 : 4), entry});
   FootprintParams fp = footprint_params(v, b, kf, pose, op);
+  fp.st = merged;
   fp.wait_flag = up.first;
   fp.wait_val = up.second;
   bool existed = false;
@@ -862,6 +890,7 @@ void op_fuse(Batch& b, const rf_kf_view* kf, const rf_pose* pose, int mode, int 
 // (k_gc_stream), or on its own before any other launch (flush_gc).
 void flush_gc(Batch& b) {
   if (b.gc_pending < 0) return;
+  flush_stream(b);  // a stream op before the GC counts the blocks the GC frees
   rf_volume* v = b.v;
   const int op = b.gc_pending;
   b.gc_pending = -1;
@@ -874,6 +903,7 @@ void flush_gc(Batch& b) {
 
 void op_gc(Batch& b) {
   rf_volume* v = b.v;
+  flush_stream(b);
   flush_gc(b);
   const int op = next_op(b);
   b.infos.push_back({3, -1});
@@ -908,6 +938,7 @@ struct BatchOutcome {
 // the ops that executed.
 rf_status batch_end(Batch& b, BatchOutcome& out) {
   rf_volume* v = b.v;
+  flush_stream(b);
   flush_gc(b);
   const int n = std::max(b.n_ops, 1);
   cudaMemcpyAsync(v->h_ops, v->d_ops, sizeof(OpCounters) * n, cudaMemcpyDeviceToHost, v->stream);
